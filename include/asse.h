@@ -1,0 +1,180 @@
+/*
+ * asse.h — C-ABI of libasse, the B200-native (sm_100a) hot path of ASSE:
+ * "Distributed super point cardinality estimation under sliding time window for
+ * high speed network" (arXiv 1807.01527). Citations: P:n = line n of the paper's
+ * PAPER.md; A<n> = reading n of DESIGN.md §2 (= SURVEY.md §8(c)).
+ *
+ * Conventions
+ *  - Every function returns asse_status (0 = OK, < 0 = error); no C++ exception
+ *    crosses the ABI. asse_last_error(ctx) returns a message for the last error.
+ *  - A context is bound to one CUDA device and one process; it is NOT thread-safe.
+ *  - The library owns every device buffer it allocates. Caller-owned memory is
+ *    marked "caller-owned" below.
+ *  - "Slice t" is the time slice being filled; asse_end_slice closes it.
+ *
+ * Device layout: AT pool codes [y][z][x][i] (u8 when 2k <= 126,
+ * else u16, A2); per-slice touch bitmap and active bitmap, g bits per ATV, in
+ * the same [y][z][x] order.
+ */
+#ifndef ASSE_H
+#define ASSE_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ASSE_OK = 0,
+  ASSE_E_PARAM = -1,     /* invalid configuration or argument */
+  ASSE_E_STATE = -2,     /* call not allowed in the current state */
+  ASSE_E_CAPACITY = -3,  /* caller buffer too small; *n_out holds the needed count */
+  ASSE_E_OVERFLOW = -4,  /* CSIP (or the restore join workspace) exceeded max_candidates */
+  ASSE_E_CUDA = -5,      /* a CUDA runtime error (message in asse_last_error) */
+  ASSE_E_PEER = -6       /* multi-GPU peers missing or inconsistent */
+} asse_status;
+
+/* Configuration (P:452 parameters; geometry reading A12). */
+typedef struct {
+  uint32_t k;              /* window length in slices, k >= 1 */
+  uint32_t n_slices;       /* slices the run may close; 0 = unbounded */
+  uint32_t r, c, u, s, g;  /* rows, column bits, frame bits, stride, ATs per ATV */
+  double theta;            /* super-point threshold, >= (A22) */
+  uint64_t seed;           /* master seed -> mangling key A (odd) and BH key (A14) */
+  uint32_t k_prime;        /* estimate window k' <= k (Alg. 1); 0 => k (A5) */
+  uint32_t max_candidates; /* CSIP capacity; also sizes the restore join workspace */
+  int32_t device;          /* CUDA device ordinal */
+  uint32_t world, rank;    /* multi-GPU: packets sharded across `world` ranks */
+} asse_config;
+
+/* One CSIP member (Alg. 4 output) with its Alg. 5 NAT and Eq. 5 estimate. */
+typedef struct {
+  uint32_t ip;             /* restored super-point candidate (f^{-1} applied) */
+  uint32_t nat;            /* NAT(ip): ATs active in all r ATVs (Alg. 5) */
+  double estimate;         /* Eq. 5 (A19); +inf when nat == g (A20) */
+  uint32_t flags;          /* ASSE_FLAG_* */
+  uint32_t pad;
+} asse_report;
+#define ASSE_FLAG_SATURATED 1u   /* nat == g */
+#define ASSE_FLAG_ABOVE_THETA 2u /* estimate >= theta */
+
+/* Per-context statistics (device times from CUDA events on the launching stream). */
+typedef struct {
+  uint64_t slices_closed;
+  uint64_t packets_scanned;      /* cumulative */
+  uint64_t kernel_launches;      /* cumulative count of this library's kernel launches */
+  uint64_t scan_launches;        /* cumulative k_scan launches */
+  double scan_ms_total;          /* cumulative k_scan device time (timing enabled only) */
+  double fold_ms_total;          /* cumulative k_fold device time (timing enabled only) */
+  uint64_t fold_launches;
+  double last_merge_ms, last_fold_ms, last_restore_ms, last_nat_ms, last_sort_ms;
+  double last_end_slice_ms;      /* device time of the whole last end_slice */
+  uint32_t last_n_super;         /* super ATVs in the last slice, all rows/frames */
+  uint32_t last_n_candidates;    /* |CSIP| of the last slice */
+  uint32_t last_n_above;         /* candidates with estimate >= theta */
+  uint32_t w_theta;              /* integer super-ATV weight threshold (A15) */
+  uint32_t code_bytes;           /* device AT code width: 1 or 2 (A2) */
+  uint32_t pad;
+} asse_stats;
+
+/* Validate a configuration (completeness/redundancy P:315-324, A10; the device
+ * path additionally needs g % 128 == 0 and g <= 512 in this version).
+ * why: caller-owned buffer of n bytes for a message (may be NULL). */
+asse_status asse_validate(const asse_config* cfg, char* why, size_t n);
+
+/* Create a context: derive keys (A14), W_theta (A15), allocate the pool with every
+ * AT = 2k (InitAT), C0 = 0, t = 0 (A3). *out receives the context. */
+asse_status asse_init(const asse_config* cfg, void** out);
+
+/* Destroy a context and free its device memory. NULL is ignored. */
+void asse_destroy(void* ctx);
+
+/* Message describing the last error on ctx (static string if ctx is NULL). */
+const char* asse_last_error(const void* ctx);
+
+/* Enable/disable per-kernel CUDA-event timing (asse_stats.*_ms). Default off. */
+asse_status asse_set_timing(void* ctx, int enable);
+
+/* Alg. 3 "Scan IP pair" for n_pairs packets of the current slice.
+ * d_pairs: caller-owned DEVICE buffer of 2*n_pairs uint32 [aip0,bip0,aip1,...]
+ *          (A33), 8-byte aligned; it must stay valid until the scan has run
+ *          (stream-ordered on `stream`; asse_end_slice synchronizes).
+ * stream:  cudaStream_t to launch on (NULL = the context's stream). The context's
+ *          stream is made to wait on it, so end_slice sees every scan (A34).
+ * Asynchronous; may be called any number of times per slice; n_pairs = 0 is legal. */
+asse_status asse_scan_slice(void* ctx, const uint32_t* d_pairs, uint64_t n_pairs, void* stream);
+
+/* Same as asse_scan_slice for a caller-owned HOST buffer (pinned for full speed):
+ * the library copies it in chunks through two device staging buffers on a copy
+ * stream, overlapping each chunk's H2D copy with the previous chunk's scan
+ * (the paper's double buffering). Returns after the last copy is issued;
+ * the host buffer must stay valid until asse_end_slice returns. */
+asse_status asse_scan_slice_host(void* ctx, const uint32_t* h_pairs, uint64_t n_pairs);
+
+/* Close slice t: (world > 1: merge the touch bitmaps of all ranks, A26), fold the
+ * slice's SetATs into the pool, weights |ATV|^{k'} and AAT, super
+ * ATVs, restore CSIP (Alg. 4), NAT + Eq. 5 (Alg. 5), sort by ip (A24), then
+ * advance to t+1 with preserveAT on the blocks whose ACT becomes 0 or k (Alg. 2).
+ * mode 0: reports with estimate >= theta (A21); mode 1: every CSIP member.
+ * h_out: caller-owned host array of cap reports (may be NULL with cap 0 to query).
+ * *n_out: number of reports produced. If cap < *n_out returns ASSE_E_CAPACITY
+ * (the slice is still closed; asse_fetch_reports re-reads the reports).
+ * ASSE_E_OVERFLOW: CSIP exceeded max_candidates; the slice is still closed and the
+ * pool advanced, *n_out = 0. ASSE_E_STATE after n_slices closed slices. Synchronous. */
+asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out,
+                           uint32_t mode);
+
+/* Re-read the reports of the last closed slice (same mode semantics). */
+asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out,
+                               uint32_t mode);
+
+/* Export the AT pool in the canonical layout [y][z][x][i], one uint16 per AT
+ * (values in [0, 2k], 2k = inactive). h_out: caller-owned host array of n entries,
+ * n must equal r * 2^u * 2^c * g. Reflects the state after the last end_slice
+ * (post-advance, A32) plus any scans issued since (not yet folded: excluded). */
+asse_status asse_export_pool(void* ctx, uint16_t* h_out, uint64_t n);
+
+/* Number of ATs in the pool (r * 2^u * 2^c * g). */
+uint64_t asse_pool_size(const void* ctx);
+
+/* Current slice index t and ACT base C0. */
+asse_status asse_get_clock(const void* ctx, uint64_t* t, uint32_t* C0);
+
+/* Keys derived from the seed (A14): A, A^{-1} mod 2^32, K_bh. For tests. */
+asse_status asse_get_keys(const void* ctx, uint32_t* A, uint32_t* A_inv, uint64_t* K_bh);
+
+/* Statistics; out: caller-owned asse_stats. */
+asse_status asse_get_stats(const void* ctx, asse_stats* out);
+
+/* The context's CUDA stream (cudaStream_t). */
+void* asse_get_stream(const void* ctx);
+
+/* Multi-GPU. world = cfg.world ranks, this rank = cfg.rank.
+ * touch[w]:  device pointers (peer-mapped, e.g. torch symmetric memory) of every
+ *            rank's per-slice touch bitmap, each asse_bitmap_bytes() long; touch[rank]
+ *            replaces this context's own touch bitmap.
+ * merged[w]: same for every rank's merged bitmap.
+ * signal[w]: every rank's signal pad (>= 256 bytes, zero-initialised) used by the
+ *            stream-ordered cross-GPU barrier when sync_mode == 0.
+ * sync_mode: 0 = device barrier over the signal pads (one process per GPU);
+ *            1 = caller-ordered (all ranks' scans complete before any merge, all
+ *                merges complete before any end_slice; used by single-GPU tests).
+ * Buffers are caller-owned and must outlive the context. */
+asse_status asse_attach_peers(void* ctx, void* const* touch, void* const* merged,
+                              void* const* signal, uint32_t sync_mode);
+
+/* Bytes of one touch bitmap (= one merged bitmap): r * 2^u * 2^c * g / 8. */
+uint64_t asse_bitmap_bytes(const void* ctx);
+
+/* Multi-GPU phase 1 of end_slice (called by asse_end_slice itself when sync_mode
+ * == 0): OR this rank's 1/world shard of every rank's touch bitmap and store the
+ * result into every rank's merged bitmap (reduce-scatter + all-gather in one
+ * peer-memory kernel). With sync_mode 1 the caller runs it for every rank, then
+ * synchronizes, then calls asse_end_slice for every rank. */
+asse_status asse_merge(void* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASSE_H */

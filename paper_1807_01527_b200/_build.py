@@ -1,0 +1,30 @@
+"""Build libasse.so in-tree for sm_100a (nvcc, static cudart)."""
+import os
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB = os.path.join(PKG, "libasse.so")
+SRCS = [os.path.join(PKG, "csrc", f) for f in ("asse_api.cu", "asse_kernels.cuh")] + [
+    os.path.join(ROOT, "include", "asse.h")]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+         "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-cudart", "static"]
+
+
+def build(force=False, verbose=False):
+    if not force and os.path.exists(LIB) and all(
+            os.path.getmtime(s) <= os.path.getmtime(LIB) for s in SRCS):
+        return LIB
+    cmd = [NVCC, *FLAGS, "-shared", "-I", os.path.join(ROOT, "include"),
+           os.path.join(PKG, "csrc", "asse_api.cu"), "-o", LIB + ".tmp"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.check_call(cmd)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    import sys
+    print(build(force=True, verbose="-v" in sys.argv))

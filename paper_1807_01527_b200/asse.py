@@ -1,0 +1,231 @@
+"""ctypes binding of libasse (include/asse.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module never
+computes anything of the method and has no CPU fallback: if libasse.so is
+missing or a CUDA call fails it raises.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libasse.so")
+
+REPORT_DTYPE = np.dtype([("ip", "<u4"), ("nat", "<u4"), ("estimate", "<f8"),
+                         ("flags", "<u4"), ("pad", "<u4")])
+FLAG_SATURATED, FLAG_ABOVE_THETA = 1, 2
+
+OK, E_PARAM, E_STATE, E_CAPACITY, E_OVERFLOW, E_CUDA, E_PEER = 0, -1, -2, -3, -4, -5, -6
+_NAMES = {E_PARAM: "ASSE_E_PARAM", E_STATE: "ASSE_E_STATE", E_CAPACITY: "ASSE_E_CAPACITY",
+          E_OVERFLOW: "ASSE_E_OVERFLOW", E_CUDA: "ASSE_E_CUDA", E_PEER: "ASSE_E_PEER"}
+
+# every symbol include/asse.h declares
+SYMBOLS = ["asse_validate", "asse_init", "asse_destroy", "asse_last_error", "asse_set_timing",
+           "asse_scan_slice", "asse_scan_slice_host", "asse_end_slice", "asse_fetch_reports",
+           "asse_export_pool", "asse_pool_size", "asse_get_clock", "asse_get_keys",
+           "asse_get_stats", "asse_get_stream", "asse_attach_peers", "asse_bitmap_bytes",
+           "asse_merge"]
+
+
+class AsseError(RuntimeError):
+    def __init__(self, status, msg=""):
+        super().__init__("%s: %s" % (_NAMES.get(status, status), msg))
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_uint32), ("n_slices", ctypes.c_uint32),
+                ("r", ctypes.c_uint32), ("c", ctypes.c_uint32), ("u", ctypes.c_uint32),
+                ("s", ctypes.c_uint32), ("g", ctypes.c_uint32), ("theta", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("k_prime", ctypes.c_uint32),
+                ("max_candidates", ctypes.c_uint32), ("device", ctypes.c_int32),
+                ("world", ctypes.c_uint32), ("rank", ctypes.c_uint32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("slices_closed", ctypes.c_uint64), ("packets_scanned", ctypes.c_uint64),
+                ("kernel_launches", ctypes.c_uint64), ("scan_launches", ctypes.c_uint64),
+                ("scan_ms_total", ctypes.c_double), ("fold_ms_total", ctypes.c_double),
+                ("fold_launches", ctypes.c_uint64),
+                ("last_merge_ms", ctypes.c_double), ("last_fold_ms", ctypes.c_double),
+                ("last_restore_ms", ctypes.c_double), ("last_nat_ms", ctypes.c_double),
+                ("last_sort_ms", ctypes.c_double), ("last_end_slice_ms", ctypes.c_double),
+                ("last_n_super", ctypes.c_uint32), ("last_n_candidates", ctypes.c_uint32),
+                ("last_n_above", ctypes.c_uint32), ("w_theta", ctypes.c_uint32),
+                ("code_bytes", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
+
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Load libasse.so (raises if it is missing — there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError("libasse.so not built (%s); run __graft_entry__.build()" % path)
+    L = ctypes.CDLL(path)
+    vp, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
+    C = ctypes.POINTER(Config)
+    sigs = {
+        "asse_validate": (i32, [C, ctypes.c_char_p, ctypes.c_size_t]),
+        "asse_init": (i32, [C, ctypes.POINTER(vp)]),
+        "asse_destroy": (None, [vp]),
+        "asse_last_error": (ctypes.c_char_p, [vp]),
+        "asse_set_timing": (i32, [vp, i32]),
+        "asse_scan_slice": (i32, [vp, vp, u64, vp]),
+        "asse_scan_slice_host": (i32, [vp, vp, u64]),
+        "asse_end_slice": (i32, [vp, vp, u32, ctypes.POINTER(u32), u32]),
+        "asse_fetch_reports": (i32, [vp, vp, u32, ctypes.POINTER(u32), u32]),
+        "asse_export_pool": (i32, [vp, vp, u64]),
+        "asse_pool_size": (u64, [vp]),
+        "asse_get_clock": (i32, [vp, ctypes.POINTER(u64), ctypes.POINTER(u32)]),
+        "asse_get_keys": (i32, [vp, ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u64)]),
+        "asse_get_stats": (i32, [vp, ctypes.POINTER(Stats)]),
+        "asse_get_stream": (vp, [vp]),
+        "asse_attach_peers": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), u32]),
+        "asse_bitmap_bytes": (u64, [vp]),
+        "asse_merge": (i32, [vp]),
+    }
+    for name, (rt, at) in sigs.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = rt, at
+    _lib = L
+    return L
+
+
+def make_config(k, r, c, u, s, g, theta, seed, k_prime=0, n_slices=0, max_candidates=1 << 20,
+                device=0, world=1, rank=0, **_):
+    return Config(k, n_slices, r, c, u, s, g, float(theta), seed, k_prime, max_candidates,
+                  device, world, rank)
+
+
+def validate(**kw):
+    why = ctypes.create_string_buffer(256)
+    cfg = make_config(**kw)
+    return load_library().asse_validate(ctypes.byref(cfg), why, 256), why.value.decode()
+
+
+class Asse:
+    """One ASSE context on one GPU. Keyword geometry as in gen.PRESETS."""
+
+    def __init__(self, **kw):
+        self._L = load_library()
+        self.cfg = make_config(**kw)
+        self.kw = dict(kw)
+        h = ctypes.c_void_p()
+        st = self._L.asse_init(ctypes.byref(self.cfg), ctypes.byref(h))
+        if st != OK:
+            raise AsseError(st, "asse_init failed (see stderr)")
+        self._h = h
+        self.r, self.c, self.u, self.g = self.cfg.r, self.cfg.c, self.cfg.u, self.cfg.g
+        self.F, self.E = 1 << self.u, 1 << self.c
+        self._cap = 0
+        self._buf = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.asse_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != OK:
+            raise AsseError(st, self._L.asse_last_error(self._h).decode())
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_timing(self, on=True):
+        self._check(self._L.asse_set_timing(self._h, 1 if on else 0))
+
+    def scan_slice(self, pairs, n=None, stream=None):
+        """pairs: device tensor (torch, uint32/int32, shape (n,2) or (2n,)) or a raw pointer."""
+        if isinstance(pairs, int):
+            ptr = pairs
+            assert n is not None
+        else:
+            ptr = pairs.data_ptr()
+            if n is None:
+                n = pairs.numel() // 2
+        self._check(self._L.asse_scan_slice(self._h, ptr, n, stream))
+
+    def scan_slice_host(self, pairs):
+        """pairs: host numpy uint32 (n,2) or a pinned torch CPU tensor."""
+        if isinstance(pairs, np.ndarray):
+            assert pairs.dtype == np.uint32 and pairs.flags.c_contiguous
+            ptr, n = pairs.ctypes.data, pairs.size // 2
+        else:
+            ptr, n = pairs.data_ptr(), pairs.numel() // 2
+        self._check(self._L.asse_scan_slice_host(self._h, ptr, n))
+
+    def _ensure(self, n):
+        if n > self._cap:
+            self._cap = max(n, 4096)
+            self._buf = np.zeros(self._cap, dtype=REPORT_DTYPE)
+
+    def end_slice(self, mode=1):
+        """Close the slice; returns the reports (numpy REPORT_DTYPE, ascending ip)."""
+        n = ctypes.c_uint32()
+        self._ensure(1)
+        st = self._L.asse_end_slice(self._h, self._buf.ctypes.data, self._cap, ctypes.byref(n), mode)
+        if st == E_CAPACITY:
+            return self.fetch_reports(mode)
+        self._check(st)
+        return self._buf[:n.value].copy()
+
+    def fetch_reports(self, mode=1):
+        n = ctypes.c_uint32()
+        st = self._L.asse_fetch_reports(self._h, None, 0, ctypes.byref(n), mode)
+        if st not in (OK, E_CAPACITY):
+            self._check(st)
+        self._ensure(n.value)
+        self._check(self._L.asse_fetch_reports(self._h, self._buf.ctypes.data, self._cap,
+                                               ctypes.byref(n), mode))
+        return self._buf[:n.value].copy()
+
+    def pool(self):
+        n = self._L.asse_pool_size(self._h)
+        out = np.empty(n, dtype=np.uint16)
+        self._check(self._L.asse_export_pool(self._h, out.ctypes.data, n))
+        return out.reshape(self.r, self.F, self.E, self.g)
+
+    def clock(self):
+        t, c0 = ctypes.c_uint64(), ctypes.c_uint32()
+        self._check(self._L.asse_get_clock(self._h, ctypes.byref(t), ctypes.byref(c0)))
+        return t.value, c0.value
+
+    def keys(self):
+        A, Ai, K = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint64()
+        self._check(self._L.asse_get_keys(self._h, ctypes.byref(A), ctypes.byref(Ai), ctypes.byref(K)))
+        return A.value, Ai.value, K.value
+
+    def stats(self):
+        s = Stats()
+        self._check(self._L.asse_get_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def stream(self):
+        return self._L.asse_get_stream(self._h)
+
+    def bitmap_bytes(self):
+        return self._L.asse_bitmap_bytes(self._h)
+
+    def attach_peers(self, touch, merged, signal=None, sync_mode=0):
+        w = len(touch)
+        arr = lambda xs: (ctypes.c_void_p * w)(*xs) if xs is not None else None
+        self._check(self._L.asse_attach_peers(self._h, arr(touch), arr(merged), arr(signal), sync_mode))
+
+    def merge(self):
+        self._check(self._L.asse_merge(self._h))

@@ -1,0 +1,708 @@
+// asse_api.cu — C-ABI of libasse (include/asse.h): context, slice state machine,
+// device memory, launches. Host code here only marshals arguments and sequences
+// kernels; every step of the hot path runs in asse_kernels.cuh.
+//
+// P:n = PAPER.md line n; A<n> = reading n of DESIGN.md §2.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "asse.h"
+#include "asse_kernels.cuh"
+
+using namespace asse;
+
+namespace {
+
+struct AboveTheta {
+  __host__ __device__ __forceinline__ bool operator()(const ReportDev& r) const {
+    return (r.flags & 2u) != 0;
+  }
+};
+
+struct Ctx {
+  asse_config cfg{};
+  // geometry
+  uint32_t F = 0, E = 0, W = 0, two_k = 0, kp = 0, a = 0, b = 0, cb = 1, wpa = 0;
+  uint32_t w_theta = 0, lpa_log2 = 0;
+  uint32_t shift[kMaxR] = {0};
+  uint64_t n_atv = 0, n_at = 0;
+  // keys (A14)
+  uint32_t A = 0, A_inv = 0;
+  uint64_t K_bh = 0;
+  // clock (A3)
+  uint32_t C0 = 0;
+  uint64_t t = 0;
+  // device
+  int device = 0, sms = 148;
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  void* pool = nullptr;
+  uint32_t* touch_own = nullptr;
+  uint32_t* touch = nullptr;        // where k_scan records (own or peer-mapped)
+  uint32_t* merged = nullptr;       // world > 1: merged bitmap of this rank
+  uint32_t* active = nullptr;
+  unsigned long long* aat = nullptr;
+  uint32_t* sa_cnt = nullptr;
+  uint32_t* sa_list = nullptr;
+  uint32_t* sa_bits = nullptr;
+  uint32_t* counters = nullptr;     // [0] n_cand [1] overflow [2] n_above [3] n_super [4] n_sel
+  uint32_t* ws = nullptr;
+  uint64_t ws_cap = 0;
+  uint32_t* cand = nullptr;
+  ReportDev* rep = nullptr;
+  ReportDev* rep_sorted = nullptr;
+  ReportDev* rep_above = nullptr;
+  uint32_t *keys = nullptr, *keys_alt = nullptr, *vals = nullptr, *vals_alt = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  uint16_t* export_buf = nullptr;
+  // host pinned
+  uint32_t* h_counters = nullptr;
+  ReportDev* h_rep = nullptr;
+  uint64_t h_rep_cap = 0;
+  // host-buffer scan staging (P:428 double buffering)
+  uint32_t* stage[2] = {nullptr, nullptr};
+  uint64_t stage_pairs = 0;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_scanned[2] = {nullptr, nullptr};
+  cudaEvent_t ev_join = nullptr;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_free;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> scan_ev;
+  cudaEvent_t ev[12] = {nullptr};
+  // last slice
+  uint32_t last_n = 0, last_above = 0;
+  bool have_reports = false;
+  // peers
+  bool peers = false;
+  uint32_t sync_mode = 0, epoch = 0;
+  void* peer_touch[kMaxWorld] = {nullptr};
+  void* peer_merged[kMaxWorld] = {nullptr};
+  void* peer_signal[kMaxWorld] = {nullptr};
+  asse_stats stats{};
+  std::string err;
+};
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      c->err = std::string(#call) + ": " + cudaGetErrorString(e_);                  \
+      return ASSE_E_CUDA;                                                           \
+    }                                                                               \
+  } while (0)
+
+#define LAUNCHED(c_) ((c_)->stats.kernel_launches++)
+
+static uint64_t splitmix_next(uint64_t* st) {  // A14
+  uint64_t z = (*st += 0x9E3779B97F4A7C15ULL);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+static uint32_t inv_newton(uint32_t A) {  // A^{-1} mod 2^32 for odd A (A8)
+  uint32_t x = A;                           // correct to 3 bits
+  for (int it = 0; it < 5; ++it) x *= 2u - A * x;
+  return x;
+}
+
+static asse_status validate(const asse_config* cfg, std::string* why) {
+  auto bad = [&](const char* m) { if (why) *why = m; return ASSE_E_PARAM; };
+  if (!cfg) return bad("null config");
+  const asse_config& p = *cfg;
+  uint32_t kp = p.k_prime ? p.k_prime : p.k;
+  if (p.k < 1) return bad("k >= 1");
+  if (kp < 1 || kp > p.k) return bad("1 <= k' <= k");
+  if (p.k > 16383) return bad("k <= 16383 (15-bit device codes)");
+  if (p.r < 2 || p.r > (uint32_t)kMaxR) return bad("2 <= r <= 8");
+  if (p.c < 2 || p.u > 16 || p.c + p.u > 32) return bad("c >= 2, u <= 16, c + u <= 32");
+  if (p.c > 24) return bad("c <= 24");
+  if (p.s < 1 || p.s > p.c) return bad("1 <= s <= c");
+  if (!(p.theta > 0)) return bad("theta > 0");
+  if (p.g < 128 || p.g > 512 || (p.g & (p.g - 1))) return bad("device path: g in {128, 256, 512}");
+  if (p.max_candidates < 1) return bad("max_candidates >= 1");
+  if (p.world < 1 || p.world > (uint32_t)kMaxWorld || p.rank >= p.world) return bad("rank < world <= 16");
+  const uint32_t W = 32 - p.u;
+  if (p.c + p.s * (p.r - 1) < W) return bad("completeness: c + s(r-1) >= 32-u (P:324, A10)");
+  std::vector<int> cover(W, 0);
+  for (uint32_t y = 0; y < p.r; ++y)
+    for (uint32_t j = 0; j < p.c; ++j) cover[(p.s * y + j) % W]++;
+  bool dup = false;
+  for (uint32_t q = 0; q < W; ++q) {
+    if (!cover[q]) return bad("completeness: an LBS bit is not covered (P:316)");
+    if (cover[q] > 1) dup = true;
+  }
+  if (!dup) return bad("redundancy: no duplicate position (P:317)");
+  return ASSE_OK;
+}
+
+static void free_all(Ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* dev[] = {c->pool, c->touch_own, c->active, c->aat, c->sa_cnt, c->sa_list, c->sa_bits,
+                 c->counters, c->ws, c->cand, c->rep, c->rep_sorted, c->rep_above, c->keys,
+                 c->keys_alt, c->vals, c->vals_alt, c->cub_tmp, c->export_buf, c->stage[0],
+                 c->stage[1]};
+  for (void* p : dev) if (p) cudaFree(p);
+  if (c->h_counters) cudaFreeHost(c->h_counters);
+  if (c->h_rep) cudaFreeHost(c->h_rep);
+  for (int q = 0; q < 2; ++q) {
+    if (c->ev_copied[q]) cudaEventDestroy(c->ev_copied[q]);
+    if (c->ev_scanned[q]) cudaEventDestroy(c->ev_scanned[q]);
+  }
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  for (auto& pr : c->scan_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto e : c->ev_free) cudaEventDestroy(e);
+  for (auto e : c->ev) if (e) cudaEventDestroy(e);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cudaStream_t st) {
+  if (n == 0) return ASSE_OK;
+  ScanParams p{};
+  p.touch = c->touch;
+  p.kbh = c->K_bh;
+  p.A = c->A;
+  p.g = c->cfg.g; p.r = c->cfg.r; p.u = c->cfg.u; p.c = c->cfg.c; p.W = c->W;
+  p.fmask = (1u << c->cfg.u) - 1u;
+  p.cmask = (1u << c->cfg.c) - 1u;
+  p.wpa = c->wpa;
+  for (int y = 0; y < kMaxR; ++y) p.shift[y] = c->shift[y];
+  uint64_t bodies = n / 2 + 1;
+  uint64_t blocks = (bodies + 255) / 256;
+  uint64_t maxb = (uint64_t)c->sms * 8;
+  if (blocks > maxb) blocks = maxb;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    if (c->ev_free.size() < 2) {
+      for (int q = 0; q < 8; ++q) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->ev_free.push_back(e);
+      }
+    }
+    e0 = c->ev_free.back(); c->ev_free.pop_back();
+    e1 = c->ev_free.back(); c->ev_free.pop_back();
+    CK(cudaEventRecord(e0, st));
+  }
+  if (c->cb == 1)
+    k_scan<1><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const uint2*>(d_pairs), n, p);
+  else
+    k_scan<2><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const uint2*>(d_pairs), n, p);
+  CK(cudaGetLastError());
+  LAUNCHED(c);
+  c->stats.scan_launches++;
+  c->stats.packets_scanned += n;
+  if (c->timing) {
+    CK(cudaEventRecord(e1, st));
+    c->scan_ev.emplace_back(e0, e1);
+  }
+  return ASSE_OK;
+}
+
+static asse_status harvest_scan_timing(Ctx* c) {
+  for (auto& pr : c->scan_ev) {
+    float ms = 0;
+    CK(cudaEventSynchronize(pr.second));
+    CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    c->stats.scan_ms_total += ms;
+    c->ev_free.push_back(pr.first);
+    c->ev_free.push_back(pr.second);
+  }
+  c->scan_ev.clear();
+  return ASSE_OK;
+}
+
+static asse_status do_merge(Ctx* c) {
+  if (!c->peers) return ASSE_OK;
+  MergeParams mp{};
+  for (uint32_t w = 0; w < c->cfg.world; ++w) {
+    mp.touch[w] = reinterpret_cast<const uint4*>(c->peer_touch[w]);
+    mp.merged[w] = reinterpret_cast<uint4*>(c->peer_merged[w]);
+  }
+  mp.world = c->cfg.world;
+  const uint64_t n4 = c->n_atv * c->wpa / 4;
+  const uint64_t per = (n4 + c->cfg.world - 1) / c->cfg.world;
+  mp.lo = per * c->cfg.rank;
+  mp.hi = std::min<uint64_t>(n4, mp.lo + per);
+  if (mp.lo >= mp.hi) return ASSE_OK;
+  uint64_t blocks = std::min<uint64_t>((mp.hi - mp.lo + 255) / 256, (uint64_t)c->sms * 4);
+  k_merge_or<<<(unsigned)blocks, 256, 0, c->stream>>>(mp);
+  CK(cudaGetLastError());
+  LAUNCHED(c);
+  return ASSE_OK;
+}
+
+static asse_status device_barrier(Ctx* c) {
+  BarrierParams bp{};
+  for (uint32_t w = 0; w < c->cfg.world; ++w) bp.pads[w] = reinterpret_cast<uint32_t*>(c->peer_signal[w]);
+  bp.world = c->cfg.world;
+  bp.rank = c->cfg.rank;
+  bp.epoch = ++c->epoch;
+  k_barrier<<<1, 32, 0, c->stream>>>(bp);
+  CK(cudaGetLastError());
+  LAUNCHED(c);
+  return ASSE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+asse_status asse_validate(const asse_config* cfg, char* why, size_t n) {
+  std::string w;
+  asse_status st = validate(cfg, &w);
+  if (why && n) snprintf(why, n, "%s", st == ASSE_OK ? "" : w.c_str());
+  return st;
+}
+
+const char* asse_last_error(const void* ctx) {
+  if (!ctx) return "no context";
+  return static_cast<const Ctx*>(ctx)->err.c_str();
+}
+
+asse_status asse_init(const asse_config* cfg, void** out) {
+  if (!out) return ASSE_E_PARAM;
+  *out = nullptr;
+  std::string why;
+  if (validate(cfg, &why) != ASSE_OK) {
+    fprintf(stderr, "asse_init: %s\n", why.c_str());
+    return ASSE_E_PARAM;
+  }
+  Ctx* c = new Ctx();
+  c->cfg = *cfg;
+  const asse_config& p = c->cfg;
+  c->F = 1u << p.u;
+  c->E = 1u << p.c;
+  c->W = 32 - p.u;
+  c->two_k = 2 * p.k;
+  c->kp = p.k_prime ? p.k_prime : p.k;
+  c->a = p.g / c->two_k;                        // P:256, A7
+  c->b = p.g - c->a * (c->two_k - 1);
+  c->cb = (c->two_k <= 126) ? 1 : 2;           // A2
+  c->wpa = p.g / 32;
+  c->lpa_log2 = (p.g == 128) ? 3 : (p.g == 256 ? 4 : 5);
+  for (uint32_t y = 0; y < p.r; ++y) c->shift[y] = (p.s * y) % c->W;
+  c->n_atv = (uint64_t)p.r * c->F * c->E;
+  c->n_at = c->n_atv * p.g;
+  // W_theta = ceil(g - g e^{-theta/g}) (A15)
+  double wt = (double)p.g - (double)p.g * exp(-p.theta / (double)p.g);
+  double wc = ceil(wt);
+  c->w_theta = (wc > (double)p.g) ? p.g + 1 : (uint32_t)wc;
+  uint64_t st = p.seed;
+  c->A = (uint32_t)(splitmix_next(&st) >> 32) | 1u;
+  c->K_bh = splitmix_next(&st);
+  c->A_inv = inv_newton(c->A);
+  c->device = p.device;
+  c->stats.w_theta = c->w_theta;
+  c->stats.code_bytes = c->cb;
+  auto fail = [&](asse_status s) {
+    fprintf(stderr, "asse_init: %s\n", c->err.c_str());
+    free_all(c);
+    delete c;
+    return s;
+  };
+#define CKI(call)                                                       \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) {                                            \
+      c->err = std::string(#call) + ": " + cudaGetErrorString(e_);      \
+      return fail(ASSE_E_CUDA);                                         \
+    }                                                                   \
+  } while (0)
+  CKI(cudaSetDevice(c->device));
+  CKI(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
+  CKI(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CKI(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  const uint64_t bm_bytes = c->n_atv * c->wpa * 4;
+  CKI(cudaMalloc(&c->pool, c->n_at * c->cb));
+  CKI(cudaMalloc(&c->touch_own, bm_bytes));
+  CKI(cudaMalloc(&c->active, bm_bytes));
+  CKI(cudaMalloc(&c->aat, (size_t)p.r * c->F * sizeof(unsigned long long)));
+  CKI(cudaMalloc(&c->sa_cnt, (size_t)p.r * c->F * 4));
+  CKI(cudaMalloc(&c->sa_list, (size_t)p.r * c->F * c->E * 4));
+  CKI(cudaMalloc(&c->sa_bits, (size_t)p.r * c->F * ((c->E + 31) / 32) * 4));
+  CKI(cudaMalloc(&c->counters, 64));
+  c->ws_cap = std::max<uint64_t>(p.max_candidates, 1u << 16);
+  CKI(cudaMalloc(&c->ws, (size_t)c->F * 2 * c->ws_cap * 4));
+  CKI(cudaMalloc(&c->cand, (size_t)p.max_candidates * 4));
+  CKI(cudaMalloc(&c->rep, (size_t)p.max_candidates * sizeof(ReportDev)));
+  CKI(cudaMalloc(&c->rep_sorted, (size_t)p.max_candidates * sizeof(ReportDev)));
+  CKI(cudaMalloc(&c->rep_above, (size_t)p.max_candidates * sizeof(ReportDev)));
+  CKI(cudaMalloc(&c->keys, (size_t)p.max_candidates * 4));
+  CKI(cudaMalloc(&c->keys_alt, (size_t)p.max_candidates * 4));
+  CKI(cudaMalloc(&c->vals, (size_t)p.max_candidates * 4));
+  CKI(cudaMalloc(&c->vals_alt, (size_t)p.max_candidates * 4));
+  {
+    size_t b1 = 0, b2 = 0;
+    cub::DoubleBuffer<uint32_t> dk(c->keys, c->keys_alt), dv(c->vals, c->vals_alt);
+    CKI(cub::DeviceRadixSort::SortPairs(nullptr, b1, dk, dv, (int)p.max_candidates, 0, 32, c->stream));
+    CKI(cub::DeviceSelect::If(nullptr, b2, c->rep_sorted, c->rep_above, c->counters + 4,
+                              (int)p.max_candidates, AboveTheta(), c->stream));
+    c->cub_bytes = std::max(b1, b2);
+    CKI(cudaMalloc(&c->cub_tmp, c->cub_bytes));
+  }
+  CKI(cudaMallocHost(&c->h_counters, 64));
+  c->h_rep_cap = 0;
+  for (auto& e : c->ev) CKI(cudaEventCreate(&e));
+  for (int q = 0; q < 2; ++q) {
+    CKI(cudaEventCreateWithFlags(&c->ev_copied[q], cudaEventDisableTiming));
+    CKI(cudaEventCreateWithFlags(&c->ev_scanned[q], cudaEventDisableTiming));
+  }
+  CKI(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  // InitAT: every AT = 2k
+  {
+    uint64_t blocks = std::min<uint64_t>((c->n_at + 255) / 256, (uint64_t)c->sms * 16);
+    if (c->cb == 1) k_fill_u8<<<(unsigned)blocks, 256, 0, c->stream>>>((uint8_t*)c->pool, (uint8_t)c->two_k, c->n_at);
+    else k_fill_u16<<<(unsigned)blocks, 256, 0, c->stream>>>((uint16_t*)c->pool, (uint16_t)c->two_k, c->n_at);
+    CKI(cudaGetLastError());
+    LAUNCHED(c);
+  }
+  CKI(cudaMemsetAsync(c->touch_own, 0, bm_bytes, c->stream));
+  CKI(cudaMemsetAsync(c->active, 0, bm_bytes, c->stream));
+  CKI(cudaStreamSynchronize(c->stream));
+  c->touch = c->touch_own;
+  c->C0 = 0;
+  c->t = 0;
+#undef CKI
+  *out = c;
+  return ASSE_OK;
+}
+
+void asse_destroy(void* ctx) {
+  if (!ctx) return;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  free_all(c);
+  delete c;
+}
+
+asse_status asse_set_timing(void* ctx, int enable) {
+  if (!ctx) return ASSE_E_PARAM;
+  static_cast<Ctx*>(ctx)->timing = enable != 0;
+  return ASSE_OK;
+}
+
+static bool closed_all(const Ctx* c) { return c->cfg.n_slices && c->t >= c->cfg.n_slices; }
+
+asse_status asse_scan_slice(void* ctx, const uint32_t* d_pairs, uint64_t n_pairs, void* stream) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (closed_all(c)) { c->err = "all n_slices closed"; return ASSE_E_STATE; }
+  if (n_pairs && (!d_pairs || ((uintptr_t)d_pairs & 7))) { c->err = "d_pairs must be 8-byte aligned device memory"; return ASSE_E_PARAM; }
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  asse_status s = launch_scan(c, d_pairs, n_pairs, st);
+  if (s != ASSE_OK) return s;
+  if (st != c->stream) {
+    CK(cudaEventRecord(c->ev_join, st));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  }
+  return ASSE_OK;
+}
+
+asse_status asse_scan_slice_host(void* ctx, const uint32_t* h_pairs, uint64_t n_pairs) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (closed_all(c)) { c->err = "all n_slices closed"; return ASSE_E_STATE; }
+  if (n_pairs == 0) return ASSE_OK;
+  if (!h_pairs) return ASSE_E_PARAM;
+  CK(cudaSetDevice(c->device));
+  if (!c->stage[0]) {
+    c->stage_pairs = 8ull << 20;  // 8 Mi pairs = 64 MiB per staging buffer
+    CK(cudaMalloc(&c->stage[0], c->stage_pairs * 8));
+    CK(cudaMalloc(&c->stage[1], c->stage_pairs * 8));
+    CK(cudaEventRecord(c->ev_scanned[0], c->stream));
+    CK(cudaEventRecord(c->ev_scanned[1], c->stream));
+  }
+  uint64_t off = 0;
+  int b = 0;
+  while (off < n_pairs) {
+    uint64_t m = std::min<uint64_t>(c->stage_pairs, n_pairs - off);
+    // the copy into stage[b] waits for the scan that last read it
+    CK(cudaStreamWaitEvent(c->copy_stream, c->ev_scanned[b], 0));
+    CK(cudaMemcpyAsync(c->stage[b], h_pairs + 2 * off, m * 8, cudaMemcpyHostToDevice, c->copy_stream));
+    CK(cudaEventRecord(c->ev_copied[b], c->copy_stream));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
+    asse_status s = launch_scan(c, c->stage[b], m, c->stream);
+    if (s != ASSE_OK) return s;
+    CK(cudaEventRecord(c->ev_scanned[b], c->stream));
+    off += m;
+    b ^= 1;
+  }
+  return ASSE_OK;
+}
+
+asse_status asse_attach_peers(void* ctx, void* const* touch, void* const* merged,
+                              void* const* signal, uint32_t sync_mode) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (c->cfg.world < 2) { c->err = "attach_peers needs world >= 2"; return ASSE_E_PEER; }
+  if (!touch || !merged || (sync_mode == 0 && !signal)) { c->err = "missing peer arrays"; return ASSE_E_PEER; }
+  for (uint32_t w = 0; w < c->cfg.world; ++w) {
+    if (!touch[w] || !merged[w] || (sync_mode == 0 && !signal[w])) { c->err = "null peer pointer"; return ASSE_E_PEER; }
+    c->peer_touch[w] = touch[w];
+    c->peer_merged[w] = merged[w];
+    c->peer_signal[w] = signal ? signal[w] : nullptr;
+  }
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  const uint64_t bm_bytes = c->n_atv * c->wpa * 4;
+  c->touch = reinterpret_cast<uint32_t*>(touch[c->cfg.rank]);
+  c->merged = reinterpret_cast<uint32_t*>(merged[c->cfg.rank]);
+  CK(cudaMemsetAsync(c->touch, 0, bm_bytes, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->sync_mode = sync_mode;
+  c->peers = true;
+  return ASSE_OK;
+}
+
+uint64_t asse_bitmap_bytes(const void* ctx) {
+  if (!ctx) return 0;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  return c->n_atv * c->wpa * 4;
+}
+
+asse_status asse_merge(void* ctx) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c->peers) { c->err = "asse_merge without attached peers"; return ASSE_E_PEER; }
+  CK(cudaSetDevice(c->device));
+  return do_merge(c);
+}
+
+static asse_status copy_reports(Ctx* c, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
+  const uint32_t n = (mode == 0) ? c->last_above : c->last_n;
+  if (n_out) *n_out = n;
+  if (!h_out || n == 0) return (h_out == nullptr && n > cap) ? ASSE_E_CAPACITY : ASSE_OK;
+  if (n > cap) return ASSE_E_CAPACITY;
+  if (c->h_rep_cap < n) {
+    if (c->h_rep) cudaFreeHost(c->h_rep);
+    c->h_rep = nullptr;
+    c->h_rep_cap = std::max<uint64_t>(n, 4096);
+    CK(cudaMallocHost(&c->h_rep, c->h_rep_cap * sizeof(ReportDev)));
+  }
+  const ReportDev* src = (mode == 0) ? c->rep_above : c->rep_sorted;
+  CK(cudaMemcpyAsync(c->h_rep, src, (size_t)n * sizeof(ReportDev), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  static_assert(sizeof(ReportDev) == sizeof(asse_report), "report layout");
+  memcpy(h_out, c->h_rep, (size_t)n * sizeof(ReportDev));
+  return ASSE_OK;
+}
+
+asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (n_out) *n_out = 0;
+  if (mode > 1) { c->err = "mode must be 0 or 1"; return ASSE_E_PARAM; }
+  if (closed_all(c)) { c->err = "all n_slices closed"; return ASSE_E_STATE; }
+  if (c->cfg.world > 1 && !c->peers) { c->err = "world > 1 requires asse_attach_peers"; return ASSE_E_PEER; }
+  CK(cudaSetDevice(c->device));
+  const asse_config& p = c->cfg;
+  cudaStream_t s = c->stream;
+  if (c->timing) CK(cudaEventRecord(c->ev[0], s));
+  // a5: merge (world > 1)
+  const uint32_t* src = c->touch;
+  if (c->peers) {
+    if (c->sync_mode == 0) {
+      asse_status st;
+      if ((st = device_barrier(c)) != ASSE_OK) return st;   // every rank's scans done
+      if ((st = do_merge(c)) != ASSE_OK) return st;
+      if ((st = device_barrier(c)) != ASSE_OK) return st;   // every shard merged
+    }
+    src = c->merged;
+  }
+  if (c->timing) CK(cudaEventRecord(c->ev[1], s));
+  // a6: fold + weights + super + preserve(t+1)
+  CK(cudaMemsetAsync(c->aat, 0, (size_t)p.r * c->F * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(c->sa_cnt, 0, (size_t)p.r * c->F * 4, s));
+  CK(cudaMemsetAsync(c->sa_bits, 0, (size_t)p.r * c->F * ((c->E + 31) / 32) * 4, s));
+  CK(cudaMemsetAsync(c->counters, 0, 64, s));
+  {
+    FoldParams fp{};
+    fp.pool = c->pool;
+    fp.touch_src = src;
+    fp.touch_zero = c->touch;
+    fp.active = c->active;
+    fp.aat = c->aat;
+    fp.sa_cnt = c->sa_cnt;
+    fp.sa_list = c->sa_list;
+    fp.sa_bits = c->sa_bits;
+    fp.n_super = c->counters + 3;
+    fp.n_chunks = c->n_at / 512;
+    fp.g = p.g; fp.k = p.k; fp.kp = c->kp; fp.C0 = c->C0; fp.a = c->a;
+    fp.c = p.c; fp.w_theta = c->w_theta; fp.lpa_log2 = c->lpa_log2;
+    uint64_t blocks = std::min<uint64_t>((fp.n_chunks + 7) / 8, (uint64_t)c->sms * 4);
+    if (c->timing) CK(cudaEventRecord(c->ev[2], s));
+    if (c->cb == 1) k_fold<1><<<(unsigned)blocks, 256, 0, s>>>(fp);
+    else k_fold<2><<<(unsigned)blocks, 256, 0, s>>>(fp);
+    CK(cudaGetLastError());
+    LAUNCHED(c);
+    c->stats.fold_launches++;
+    if (c->timing) CK(cudaEventRecord(c->ev[3], s));
+  }
+  // a7: restore (Alg. 4), one CTA per frame
+  {
+    RestoreParams rp{};
+    rp.sa_cnt = c->sa_cnt; rp.sa_list = c->sa_list; rp.sa_bits = c->sa_bits;
+    rp.ws = c->ws; rp.ws_cap = c->ws_cap;
+    rp.cand = c->cand; rp.n_cand = c->counters + 0; rp.overflow = c->counters + 1;
+    rp.max_cand = p.max_candidates;
+    rp.r = p.r; rp.u = p.u; rp.c = p.c; rp.W = c->W; rp.F = c->F;
+    std::vector<uint8_t> known(c->W, 0);
+    for (uint32_t y = 0; y < p.r; ++y) {
+      rp.shift[y] = c->shift[y];
+      uint32_t ov = 0, nf = 0;
+      for (uint32_t j = 0; j < p.c; ++j) {
+        uint32_t pos = (c->shift[y] + j) % c->W;
+        if (known[pos]) ov |= 1u << j;
+        else rp.freepos[y][nf++] = (uint8_t)j;
+      }
+      for (uint32_t j = 0; j < p.c; ++j) known[(c->shift[y] + j) % c->W] = 1;
+      rp.ov[y] = ov;
+      rp.nfree[y] = nf;
+      rp.use_enum_max[y] = (nf <= 20) ? 4u : 0u;
+    }
+    size_t smem = (size_t)p.r * ((c->E + 31) / 32) * 4;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (c->timing) CK(cudaEventRecord(c->ev[4], s));
+    k_restore<<<c->F, 512, smem, s>>>(rp);
+    CK(cudaGetLastError());
+    LAUNCHED(c);
+    if (c->timing) CK(cudaEventRecord(c->ev[5], s));
+  }
+  CK(cudaMemcpyAsync(c->h_counters, c->counters, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint32_t n_cand_raw = c->h_counters[0];
+  const bool overflow = c->h_counters[1] != 0 || n_cand_raw > p.max_candidates;
+  const uint32_t n_cand = overflow ? 0 : n_cand_raw;
+  // a8: NAT + Eq. 5, sort by ip, compaction of est >= theta
+  if (c->timing) CK(cudaEventRecord(c->ev[6], s));
+  if (n_cand > 0) {
+    NatParams np{};
+    np.cand = c->cand; np.active = c->active; np.aat = c->aat; np.reports = c->rep;
+    np.keys = c->keys; np.vals = c->vals; np.n_above = c->counters + 2; np.n = n_cand;
+    np.A_inv = c->A_inv; np.r = p.r; np.u = p.u; np.c = p.c; np.W = c->W; np.F = c->F;
+    np.g = p.g; np.wpa = c->wpa; np.theta = p.theta; np.cells = (double)p.g * (double)c->E;
+    for (int y = 0; y < kMaxR; ++y) np.shift[y] = c->shift[y];
+    unsigned blocks = (unsigned)std::min<uint64_t>((n_cand + 255) / 256, (uint64_t)c->sms * 8);
+    k_nat_est<<<blocks, 256, 0, s>>>(np);
+    CK(cudaGetLastError());
+    LAUNCHED(c);
+  }
+  if (c->timing) CK(cudaEventRecord(c->ev[7], s));
+  if (n_cand > 0) {
+    cub::DoubleBuffer<uint32_t> dk(c->keys, c->keys_alt), dv(c->vals, c->vals_alt);
+    size_t bytes = c->cub_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, dk, dv, (int)n_cand, 0, 32, s));
+    c->stats.kernel_launches += 4;  // onesweep radix passes (count is indicative)
+    unsigned blocks = (unsigned)std::min<uint64_t>((n_cand + 255) / 256, (uint64_t)c->sms * 8);
+    k_gather<<<blocks, 256, 0, s>>>(c->rep, dv.Current(), n_cand, c->rep_sorted);
+    CK(cudaGetLastError());
+    LAUNCHED(c);
+    bytes = c->cub_bytes;
+    CK(cub::DeviceSelect::If(c->cub_tmp, bytes, c->rep_sorted, c->rep_above, c->counters + 4,
+                             (int)n_cand, AboveTheta(), s));
+    c->stats.kernel_launches += 2;
+  }
+  if (c->timing) CK(cudaEventRecord(c->ev[8], s));
+  CK(cudaMemcpyAsync(c->h_counters, c->counters, 32, cudaMemcpyDeviceToHost, s));
+  if (c->timing) CK(cudaEventRecord(c->ev[9], s));
+  CK(cudaStreamSynchronize(s));
+  c->last_n = n_cand;
+  c->last_above = n_cand ? c->h_counters[4] : 0;
+  c->have_reports = true;
+  c->stats.last_n_super = c->h_counters[3];
+  c->stats.last_n_candidates = n_cand_raw;
+  c->stats.last_n_above = c->last_above;
+  if (c->timing) {
+    float ms;
+    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1])); c->stats.last_merge_ms = ms;
+    CK(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3])); c->stats.last_fold_ms = ms;
+    c->stats.fold_ms_total += ms;
+    CK(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5])); c->stats.last_restore_ms = ms;
+    CK(cudaEventElapsedTime(&ms, c->ev[6], c->ev[7])); c->stats.last_nat_ms = ms;
+    CK(cudaEventElapsedTime(&ms, c->ev[7], c->ev[8])); c->stats.last_sort_ms = ms;
+    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[9])); c->stats.last_end_slice_ms = ms;
+    asse_status hs = harvest_scan_timing(c);
+    if (hs != ASSE_OK) return hs;
+  }
+  // a9: advance; preserveAT for t+1 already applied by k_fold (Alg. 2)
+  c->t += 1;
+  c->C0 = (uint32_t)(c->t % c->two_k);
+  c->stats.slices_closed++;
+  if (overflow) {
+    c->last_n = c->last_above = 0;
+    c->err = "CSIP exceeded max_candidates (or the restore join workspace)";
+    return ASSE_E_OVERFLOW;
+  }
+  return copy_reports(c, h_out, cap, n_out, mode);
+}
+
+asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c->have_reports) { c->err = "no closed slice"; return ASSE_E_STATE; }
+  if (mode > 1) return ASSE_E_PARAM;
+  CK(cudaSetDevice(c->device));
+  return copy_reports(c, h_out, cap, n_out, mode);
+}
+
+uint64_t asse_pool_size(const void* ctx) {
+  return ctx ? static_cast<const Ctx*>(ctx)->n_at : 0;
+}
+
+asse_status asse_export_pool(void* ctx, uint16_t* h_out, uint64_t n) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!h_out || n != c->n_at) { c->err = "export_pool: n must equal asse_pool_size()"; return ASSE_E_PARAM; }
+  CK(cudaSetDevice(c->device));
+  if (c->cb == 2) {
+    CK(cudaMemcpyAsync(h_out, c->pool, n * 2, cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    if (!c->export_buf) CK(cudaMalloc(&c->export_buf, n * 2));
+    uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)c->sms * 16);
+    k_export_u8<<<(unsigned)blocks, 256, 0, c->stream>>>((const uint8_t*)c->pool, c->export_buf, n);
+    CK(cudaGetLastError());
+    LAUNCHED(c);
+    CK(cudaMemcpyAsync(h_out, c->export_buf, n * 2, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return ASSE_OK;
+}
+
+asse_status asse_get_clock(const void* ctx, uint64_t* t, uint32_t* C0) {
+  if (!ctx) return ASSE_E_PARAM;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (t) *t = c->t;
+  if (C0) *C0 = c->C0;
+  return ASSE_OK;
+}
+
+asse_status asse_get_keys(const void* ctx, uint32_t* A, uint32_t* A_inv, uint64_t* K_bh) {
+  if (!ctx) return ASSE_E_PARAM;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (A) *A = c->A;
+  if (A_inv) *A_inv = c->A_inv;
+  if (K_bh) *K_bh = c->K_bh;
+  return ASSE_OK;
+}
+
+asse_status asse_get_stats(const void* ctx, asse_stats* out) {
+  if (!ctx || !out) return ASSE_E_PARAM;
+  *out = static_cast<const Ctx*>(ctx)->stats;
+  return ASSE_OK;
+}
+
+void* asse_get_stream(const void* ctx) {
+  return ctx ? (void*)static_cast<const Ctx*>(ctx)->stream : nullptr;
+}
+
+}  // extern "C"

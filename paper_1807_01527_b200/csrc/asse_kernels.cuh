@@ -1,0 +1,595 @@
+// asse_kernels.cuh — sm_100a kernels of the ASSE hot path (arXiv 1807.01527).
+//
+// P:n = PAPER.md line n; A<n> = reading n of DESIGN.md §2. No tensor cores: nothing
+// here is a dense contraction. Layout:
+//   pool    : AT codes [y][z][x][i], CT = uint8_t (2k <= 126) or uint16_t   (A2)
+//   touch   : per-slice SetAT record, g bits per ATV, same [y][z][x] order;
+//             bit of AT i inside word i>>5 permuted (touch_bit) for a PRMT fold
+//   active  : checkAT(k') result of the last end_slice, g bits per ATV
+// The value SetAT writes into AT i during slice t is fully determined by i and t
+// (block ACT (C0 + blk(i)) mod 2k), so the scan only records WHICH ATs were
+// set (1 bit each, L2-resident) and k_fold writes the codes once per slice.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace asse {
+
+constexpr int kMaxR = 8;       // rows supported by the device path
+constexpr int kMaxWorld = 16;  // ranks supported by the peer merge
+
+// ------------------------------------------------------------------ helpers
+
+__device__ __forceinline__ uint32_t bh_index(uint32_t bip, uint64_t kbh, uint32_t g) {
+  // BH (A13): SplitMix64 finalizer of bip ^ K_bh, multiply-shift to [0, g)
+  uint64_t z = (uint64_t)bip ^ kbh;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return (uint32_t)(((z >> 32) * (uint64_t)g) >> 32);
+}
+
+// Bit position of AT i inside touch word i>>5. Lane l of k_fold owns ATs
+// 16l..16l+15 of a 512-AT chunk, i.e. half-word (i>>4)&1 of word i>>5; inside
+// that half the order makes a PRMT selector one shift + one mask away.
+template <int CB>
+__device__ __forceinline__ uint32_t touch_bit(uint32_t i) {
+  uint32_t half = ((i >> 4) & 1u) << 4;
+  if (CB == 1) return half + 4u * (i & 3u) + ((i >> 2) & 3u);   // code 4q+j -> bit 4j+q
+  return half + 8u * (i & 1u) + ((i >> 1) & 7u);                // code 2q+j -> bit 8j+q
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// streaming read-only input (packets): no L1 allocation, evict-first in L2
+__device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  return r;
+}
+// AT pool streamed once per slice: evict-first so the bitmaps stay L2-resident
+__device__ __forceinline__ uint4 ld_pool(const uint4* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_pool(uint4* p, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
+}
+
+// ------------------------------------------------------------------- scan
+
+struct ScanParams {
+  uint32_t* touch;        // touch bitmap, words_per_atv words per ATV
+  uint64_t kbh;           // BH key
+  uint32_t A;             // mangling key (A8)
+  uint32_t g, r, u, c, W; // W = 32 - u
+  uint32_t fmask, cmask;
+  uint32_t wpa;           // touch words per ATV = g/32
+  uint32_t shift[kMaxR];  // (s*y) mod W
+};
+
+// Alg. 3 for one pair: RRH(aip) -> r ATVs <x_y, y, z>, i = BH(bip),
+// SetAT recorded as touch bit i of each ATV.
+template <int CB>
+__device__ __forceinline__ void scan_pair(const ScanParams& p, uint32_t aip, uint32_t bip) {
+  const uint32_t h = p.A * aip;                        // f(aip) = A*aip mod 2^32
+  const uint32_t z = h & p.fmask;                      // Z(aip) = RBS(f, u)
+  const uint64_t L = (uint64_t)(h >> p.u);             // LBS(f, 32-u)
+  const uint64_t D = L | (L << p.W);                   // wrap-around view
+  const uint32_t i = bh_index(bip, p.kbh, p.g);
+  const uint32_t wofs = i >> 5;
+  const uint32_t bit = 1u << touch_bit<CB>(i);
+  const uint32_t yz0 = z << p.c;
+#pragma unroll
+  for (int y = 0; y < kMaxR; ++y) {
+    if (y < (int)p.r) {
+      uint32_t x = (uint32_t)(D >> p.shift[y]) & p.cmask;
+      uint32_t atv = ((uint32_t)y << (p.u + p.c)) + yz0 + x;   // ((y*F + z) << c) | x
+      atomicOr(p.touch + (size_t)atv * p.wpa + wofs, bit);    // RED.E.OR (no return)
+    }
+  }
+}
+
+template <int CB>
+__global__ void __launch_bounds__(256) k_scan(const uint2* __restrict__ pk, uint64_t n,
+                                              ScanParams p) {
+  // head / tail packets when the buffer is not 16-byte aligned or n is odd
+  const uint32_t head = (((uintptr_t)pk) & 15u) ? 1u : 0u;
+  const uint64_t nb = (n > head) ? (n - head) >> 1 : 0;  // uint4 bodies (2 packets each)
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  if (tid == 0) {
+    if (head && n > 0) scan_pair<CB>(p, pk[0].x, pk[0].y);
+    if (n > head && ((n - head) & 1)) scan_pair<CB>(p, pk[n - 1].x, pk[n - 1].y);
+  }
+  const uint4* body = reinterpret_cast<const uint4*>(pk + head);
+  const uint64_t pol = policy_evict_first();
+  uint64_t q = tid;
+  for (; q + nthr < nb; q += 2 * nthr) {
+    uint4 v0 = ld_stream(body + q, pol);
+    uint4 v1 = ld_stream(body + q + nthr, pol);
+    scan_pair<CB>(p, v0.x, v0.y);
+    scan_pair<CB>(p, v0.z, v0.w);
+    scan_pair<CB>(p, v1.x, v1.y);
+    scan_pair<CB>(p, v1.z, v1.w);
+  }
+  if (q < nb) {
+    uint4 v0 = ld_stream(body + q, pol);
+    scan_pair<CB>(p, v0.x, v0.y);
+    scan_pair<CB>(p, v0.z, v0.w);
+  }
+}
+
+// ------------------------------------------------------------------- fold
+
+struct FoldParams {
+  void* pool;                 // codes
+  const uint32_t* touch_src;  // touch bits to fold (local, or the merged bitmap)
+  uint32_t* touch_zero;       // touch bitmap to clear for the next slice
+  uint32_t* active;           // out: active bits (same layout family)
+  unsigned long long* aat;    // out: AAT[y][z], pre-zeroed
+  uint32_t* sa_cnt;           // out: |SA(y,z)|, pre-zeroed
+  uint32_t* sa_list;          // out: SA(y,z) columns, E per (y,z)
+  uint32_t* sa_bits;          // out: SA(y,z) membership bits, pre-zeroed
+  uint32_t* n_super;          // out: total super ATVs
+  uint64_t n_chunks;          // pool ATs / 512
+  uint32_t g, k, kp, C0, a;   // ATV size, window, k', ACT base, block size a (A7)
+  uint32_t c, w_theta;        // column bits, integer super threshold (A15)
+  uint32_t lpa_log2;          // log2(lanes per ATV) = log2(g/16)
+};
+
+// Element-wise SWAR constants: CB = 1 -> 4 x 7-bit codes per word (guard bit 7),
+// CB = 2 -> 2 x 15-bit codes per word (guard bit 15).
+template <int CB> struct Swar;
+template <> struct Swar<1> {
+  static constexpr int NW = 4;      // words per lane (16 codes)
+  static constexpr int EPW = 4;     // elements per word
+  static constexpr int EB = 8;      // element bits
+  static constexpr uint32_t G = 0x80808080u;
+  static constexpr uint32_t SIGN = 0xBA98u;  // PRMT: replicate the msb of every byte
+  static constexpr uint32_t EMPTY_LO = 127u;
+};
+template <> struct Swar<2> {
+  static constexpr int NW = 8;
+  static constexpr int EPW = 2;
+  static constexpr int EB = 16;
+  static constexpr uint32_t G = 0x80008000u;
+  static constexpr uint32_t SIGN = 0xBB99u;  // replicate the msb of each half-word
+  static constexpr uint32_t EMPTY_LO = 32767u;
+};
+
+// v in [lo, hi] per element, result in the guard bits (borrow-free: vx elements have
+// the guard bit set and lo <= guard-1; HX = hi | guard, v <= guard - 2).
+__device__ __forceinline__ uint32_t in_range(uint32_t vx, uint32_t v, uint32_t LO, uint32_t HX) {
+  return (vx - LO) & (HX - v);
+}
+
+// One 512-AT chunk per warp and pass; lane l owns ATs 16l..16l+15 (16 B of u8 or
+// 32 B of u16 codes). For every AT:
+//   SetAT fold  v <- ACT(i) if touched this slice                     (Alg. 3)
+//   checkAT     active <=> v != 2k and (ACT(i) - v) mod 2k <= k'-1    (Alg. 1)
+//   weight      |ATV|^{k'} = popcount over the ATV; AAT
+//   super       w >= W_theta -> SA(y,z)
+//   preserveAT  for slice t+1 on ATs whose block ACT becomes 0 or k  (Alg. 2)
+// The per-AT constants depend only on the AT index, so each lane computes them
+// once per launch and keeps them in registers (blocked warp -> chunk mapping).
+template <int CB>
+__global__ void __launch_bounds__(256) k_fold(FoldParams p) {
+  using S = Swar<CB>;
+  constexpr int NW = S::NW, EPW = S::EPW, EB = S::EB;
+  constexpr uint32_t G = S::G;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lpa = 1u << p.lpa_log2;            // lanes per ATV (8, 16, 32)
+  const uint32_t lia = lane & (lpa - 1u);           // lane within its ATV
+  const uint32_t two_k = 2u * p.k;
+
+  // ---- per-lane, per-element constants (positions i = 16*lia + e)
+  uint32_t CLK[NW], LO1[NW], HI1[NW], LO2[NW], HI2[NW], LE1[NW], HE1[NW], LE2[NW], HE2[NW];
+  uint32_t swept_mask = 0;  // bit q: word q holds ATs of a block swept for t+1
+#pragma unroll
+  for (int q = 0; q < NW; ++q) {
+    CLK[q] = LO1[q] = HI1[q] = LO2[q] = HI2[q] = LE1[q] = HE1[q] = LE2[q] = HE2[q] = 0;
+#pragma unroll
+    for (int e = 0; e < EPW; ++e) {
+      const uint32_t i = 16u * lia + (uint32_t)(q * EPW + e);
+      uint32_t blk = (p.a > 0) ? min(i / p.a, two_k - 1u) : two_k - 1u;  // A7
+      uint32_t clk = (p.C0 + blk) % two_k;
+      uint32_t lo1, hi1 = clk, lo2, hi2;
+      if (clk + 1u >= p.kp) { lo1 = clk + 1u - p.kp; lo2 = S::EMPTY_LO; hi2 = 0; }
+      else { lo1 = 0; lo2 = clk + 1u + two_k - p.kp; hi2 = two_k - 1u; }
+      // Alg. 2 for the new ACT of slice t+1
+      uint32_t nclk = (clk + 1u == two_k) ? 0u : clk + 1u;
+      uint32_t le1 = S::EMPTY_LO, he1 = 0, le2 = S::EMPTY_LO, he2 = 0;
+      if (nclk == 0) { le1 = 0; he1 = p.k; }                         // 0 <= at <= k
+      else if (nclk == p.k) { le1 = p.k; he1 = two_k - 1u; le2 = 0; he2 = 0; }  // k..2k-1, 0
+      if (le1 <= he1 || le2 <= he2) swept_mask |= 1u << q;
+      const uint32_t sh = (uint32_t)e * EB;
+      const uint32_t gbit = 1u << (EB - 1);
+      CLK[q] |= clk << sh;
+      LO1[q] |= lo1 << sh; HI1[q] |= (hi1 | gbit) << sh;
+      LO2[q] |= lo2 << sh; HI2[q] |= (hi2 | gbit) << sh;
+      LE1[q] |= le1 << sh; HE1[q] |= (he1 | gbit) << sh;
+      LE2[q] |= le2 << sh; HE2[q] |= (he2 | gbit) << sh;
+    }
+  }
+  // warp-uniform: words that need the erase step in any lane
+  swept_mask = __reduce_or_sync(0xFFFFFFFFu, swept_mask);
+  uint32_t TWOK = 0;
+#pragma unroll
+  for (int e = 0; e < EPW; ++e) TWOK |= two_k << (e * EB);
+
+  // ---- blocked chunk range of this warp
+  const uint64_t warp_global = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t per = (p.n_chunks + n_warps - 1) / n_warps;
+  const uint64_t c0 = warp_global * per;
+  const uint64_t c1 = min(p.n_chunks, c0 + per);
+  if (c0 >= c1) return;
+
+  constexpr int LANE_WORDS = NW;  // uint32 words of codes per lane
+  const uint64_t pol = policy_evict_first();
+  uint4* pool4 = reinterpret_cast<uint4*>(p.pool);
+  const uint32_t tshift = (lane & 1u) << 4;
+  const uint32_t atvs_per_chunk_log2 = 5u - p.lpa_log2;
+  const uint32_t E = 1u << p.c;
+
+  uint32_t cur[LANE_WORDS], nxt[LANE_WORDS];
+  uint32_t tw_cur, tw_nxt = 0;
+  auto load = [&](uint64_t ch, uint32_t* dst, uint32_t& tw) {
+    const uint4* src = pool4 + (ch * 32u + lane) * (LANE_WORDS / 4);
+#pragma unroll
+    for (int v = 0; v < LANE_WORDS / 4; ++v) {
+      uint4 t4 = ld_pool(src + v, pol);
+      dst[4 * v + 0] = t4.x; dst[4 * v + 1] = t4.y; dst[4 * v + 2] = t4.z; dst[4 * v + 3] = t4.w;
+    }
+    tw = __ldcg(p.touch_src + ch * 16u + (lane >> 1));
+  };
+  load(c0, cur, tw_cur);
+
+  unsigned long long aat_acc = 0;
+  uint32_t aat_yz = 0xFFFFFFFFu;
+  uint32_t nsup = 0;
+
+  for (uint64_t ch = c0; ch < c1; ++ch) {
+    if (ch + 1 < c1) load(ch + 1, nxt, tw_nxt);
+    const uint32_t field = (tw_cur >> tshift) & 0xFFFFu;
+    uint32_t v[LANE_WORDS];
+    uint32_t cnt = 0, accbits = 0;
+    bool changed = false;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      // SetAT fold via PRMT: element e takes byte(s) of CLK when its touch bit is set
+      uint32_t sel;
+      if (CB == 1) {
+        uint32_t f = (q <= 2) ? (field << (2 - q)) : (field >> (q - 2));
+        sel = 0x3210u | (f & 0x4444u);
+      } else {
+        sel = 0x3210u | (((field >> q) & 0x0101u) * 0x44u);
+      }
+      uint32_t x = __byte_perm(cur[q], CLK[q], sel);
+      // checkAT (Alg. 1): two intervals of the cyclic window
+      uint32_t vx = x | G;
+      uint32_t act = (in_range(vx, x, LO1[q], HI1[q]) | in_range(vx, x, LO2[q], HI2[q])) & G;
+      cnt += __popc(act);
+      if (CB == 1) accbits |= act >> (7 - q);
+      else accbits |= act >> (15 - q);
+      // preserveAT for slice t+1 (Alg. 2), only in words holding swept blocks
+      if (swept_mask & (1u << q)) {
+        uint32_t er = (in_range(vx, x, LE1[q], HE1[q]) | in_range(vx, x, LE2[q], HE2[q])) & G;
+        uint32_t m = __byte_perm(er, 0u, S::SIGN);
+        x = (x & ~m) | (TWOK & m);
+      }
+      changed |= (x != cur[q]);
+      v[q] = x;
+    }
+    // write back only the 16/32-byte lane slices that changed
+    if (changed) {
+      uint4* dst = pool4 + (ch * 32u + lane) * (LANE_WORDS / 4);
+#pragma unroll
+      for (int w4 = 0; w4 < LANE_WORDS / 4; ++w4)
+        st_pool(dst + w4, make_uint4(v[4 * w4], v[4 * w4 + 1], v[4 * w4 + 2], v[4 * w4 + 3]), pol);
+    }
+    // active word = even lane bits | odd lane bits shifted into the free positions
+    uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, accbits, 1);
+    if ((lane & 1u) == 0) {
+      uint32_t word = (CB == 1) ? (accbits | (other << 4)) : (accbits | (other << 8));
+      p.active[ch * 16u + (lane >> 1)] = word;
+      p.touch_zero[ch * 16u + (lane >> 1)] = 0u;
+    }
+    // weight of each ATV in the chunk: reduce over its lpa lanes
+    uint32_t w = cnt;
+    for (uint32_t off = lpa >> 1; off > 0; off >>= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, off);
+    const uint64_t atv = (ch << atvs_per_chunk_log2) + (lane >> p.lpa_log2);
+    const uint32_t yz = (uint32_t)(atv >> p.c);
+    const uint32_t xcol = (uint32_t)atv & (E - 1u);
+    if (lia == 0 && w >= p.w_theta) {            // super ATV
+      uint32_t slot = atomicAdd(p.sa_cnt + yz, 1u);
+      p.sa_list[(size_t)yz * E + slot] = xcol;
+      atomicOr(p.sa_bits + (((size_t)yz * E + xcol) >> 5), 1u << (xcol & 31u));
+      nsup++;
+    }
+    // AAT: the whole chunk lies in one (y, z) slab (E*g >= 512)
+    uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    if (yz != aat_yz) {
+      if (aat_yz != 0xFFFFFFFFu && lane == 0 && aat_acc) atomicAdd(p.aat + aat_yz, aat_acc);
+      aat_yz = yz;
+      aat_acc = 0;
+    }
+    aat_acc += tot;
+#pragma unroll
+    for (int q = 0; q < LANE_WORDS; ++q) cur[q] = nxt[q];
+    tw_cur = tw_nxt;
+  }
+  if (lane == 0 && aat_acc) atomicAdd(p.aat + aat_yz, aat_acc);
+  nsup = __reduce_add_sync(0xFFFFFFFFu, nsup);
+  if (lane == 0 && nsup) atomicAdd(p.n_super, nsup);
+}
+
+// ---------------------------------------------------------------- restore
+
+struct RestoreParams {
+  const uint32_t* sa_cnt;   // [r*F]
+  const uint32_t* sa_list;  // [r*F][E]
+  const uint32_t* sa_bits;  // [r*F][E/32]
+  uint32_t* ws;             // join workspace: F frames x 2 buffers x ws_cap
+  uint64_t ws_cap;
+  uint32_t* cand;           // out: candidates as mangled values h = (LBS << u) | z
+  uint32_t* n_cand;         // out: |CSIP|
+  uint32_t* overflow;       // out: 1 if CSIP or a join level exceeded its capacity
+  uint32_t max_cand;
+  uint32_t r, u, c, W, F;
+  uint32_t shift[kMaxR];    // (s*y) mod W
+  uint32_t ov[kMaxR];       // bits of x_y already fixed by rows < y
+  uint32_t nfree[kMaxR];    // c - popc(ov[y])
+  uint32_t use_enum_max[kMaxR];  // enumerate the 2^nfree completions when 2^nfree <= this * |SA|
+  uint8_t freepos[kMaxR][32];    // free bit positions of x_y
+};
+
+__device__ __forceinline__ uint32_t place_row(uint32_t x, uint32_t sh, uint32_t W) {
+  // LBS bits (sh + j) mod W <- x[j] (P:324 wrap-around)
+  uint64_t P = (uint64_t)x << sh;
+  uint32_t wmask = (W >= 32) ? 0xFFFFFFFFu : ((1u << W) - 1u);
+  return (uint32_t)((P | (P >> W)) & wmask);
+}
+
+// Alg. 4 per frame z (one CTA): CSIP_z = {LBS : x_y(LBS) in SA(y, z) for all y}.
+// The r-fold product of P:364 is evaluated as a join: rows are added one at a time,
+// and a partial LBS only survives when every duplicate position agrees,
+// which yields exactly the tuples that pass Alg. 4's check (A16). Row y either scans
+// SA(y,z) comparing the already-fixed bits, or enumerates the 2^nfree completions of
+// x_y and tests SA membership — whichever is fewer probes.
+__global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
+  extern __shared__ uint32_t s_bits[];  // r * E/32 words of SA(y, z) membership
+  __shared__ uint32_t s_next;
+  __shared__ uint32_t s_nin;
+  const uint32_t z = blockIdx.x;
+  const uint32_t E = 1u << p.c;
+  const uint32_t ew = (E + 31u) >> 5;
+  const uint32_t cmask = (p.c >= 32) ? 0xFFFFFFFFu : ((1u << p.c) - 1u);
+  for (uint32_t q = threadIdx.x; q < p.r * ew; q += blockDim.x) {
+    uint32_t y = q / ew, w = q % ew;
+    s_bits[q] = p.sa_bits[((size_t)y * p.F + z) * ew + w];
+  }
+  uint32_t* buf[2] = {p.ws + (size_t)z * 2 * p.ws_cap, p.ws + (size_t)z * 2 * p.ws_cap + p.ws_cap};
+  if (threadIdx.x == 0) { s_nin = 1; buf[0][0] = 0; }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint32_t y = 0; y < p.r; ++y) {
+    const uint32_t n_in = s_nin;
+    const uint32_t nsa = p.sa_cnt[y * p.F + z];
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+    if (n_in == 0 || nsa == 0) {
+      if (threadIdx.x == 0) s_nin = 0;
+      __syncthreads();
+      break;
+    }
+    const bool last = (y + 1 == p.r);
+    const uint32_t nf = p.nfree[y];
+    const bool use_enum = ((1ull << nf) <= (uint64_t)p.use_enum_max[y] * nsa);
+    const uint64_t per = use_enum ? (1ull << nf) : (uint64_t)nsa;
+    const uint64_t total = (uint64_t)n_in * per;
+    const uint32_t* in = buf[y & 1];
+    uint32_t* out = buf[(y + 1) & 1];
+    const uint32_t* sal = p.sa_list + ((size_t)y * p.F + z) * E;
+    const uint32_t* bits = s_bits + y * ew;
+    const uint64_t rounded = (total + 31u) & ~31ull;
+    for (uint64_t idx = threadIdx.x; idx < rounded; idx += blockDim.x) {
+      bool ok = false;
+      uint32_t nl = 0;
+      if (idx < total) {
+        const uint32_t L = in[idx / per];
+        const uint32_t sub = (uint32_t)(idx % per);
+        const uint64_t D = (uint64_t)L | ((uint64_t)L << p.W);
+        const uint32_t xk = (uint32_t)(D >> p.shift[y]) & cmask;
+        uint32_t x;
+        if (use_enum) {
+          x = xk & p.ov[y];
+          for (uint32_t b = 0; b < nf; ++b) x |= ((sub >> b) & 1u) << p.freepos[y][b];
+          ok = (bits[x >> 5] >> (x & 31u)) & 1u;
+        } else {
+          x = sal[sub];
+          ok = ((x ^ xk) & p.ov[y]) == 0;
+        }
+        nl = L | place_row(x, p.shift[y], p.W);
+      }
+      // warp-aggregated append
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
+      if (m) {
+        const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+        uint32_t base = 0;
+        const uint32_t leader = __ffs(m) - 1;
+        if (last) {
+          if (lane == leader) base = atomicAdd(p.n_cand, __popc(m));
+          base = __shfl_sync(0xFFFFFFFFu, base, leader);
+          if (ok) {
+            uint32_t slot = base + rank;
+            if (slot < p.max_cand) p.cand[slot] = (p.u ? (nl << p.u) : nl) | z;
+            else *p.overflow = 1u;
+          }
+        } else {
+          if (lane == leader) base = atomicAdd(&s_next, __popc(m));
+          base = __shfl_sync(0xFFFFFFFFu, base, leader);
+          if (ok) {
+            uint32_t slot = base + rank;
+            if (slot < p.ws_cap) out[slot] = nl;
+            else *p.overflow = 1u;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_nin = (uint32_t)min((uint64_t)s_next, p.ws_cap);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ NAT + Eq. 5
+
+struct NatParams {
+  const uint32_t* cand;        // mangled values h
+  const uint32_t* active;      // active bits, wpa words per ATV
+  const unsigned long long* aat;
+  void* reports;               // asse_report[n] (ip, nat, estimate, flags, pad)
+  uint32_t* keys;              // ip, for the sort
+  uint32_t* vals;              // index, for the sort
+  uint32_t* n_above;
+  uint32_t n;
+  uint32_t A_inv, r, u, c, W, F, g, wpa;
+  double theta, cells;         // cells = g * 2^c
+  uint32_t shift[kMaxR];
+};
+
+struct ReportDev { uint32_t ip, nat; double estimate; uint32_t flags, pad; };
+
+// Alg. 5 NAT as an AND of the r active bit rows + popcount, UP (Eq. 4,
+// P:412) from AAT in double, Eq. 5 (A19), flags (A20, A21).
+__global__ void __launch_bounds__(256) k_nat_est(NatParams p) {
+  const uint32_t fmask = (1u << p.u) - 1u;
+  const uint32_t cmask = (1u << p.c) - 1u;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < p.n; q += gridDim.x * blockDim.x) {
+    const uint32_t h = p.cand[q];
+    const uint32_t z = h & fmask;
+    const uint64_t L = (uint64_t)(h >> p.u);
+    const uint64_t D = L | (L << p.W);
+    const uint4* rows[kMaxR];
+#pragma unroll
+    for (int y = 0; y < kMaxR; ++y) {
+      if (y < (int)p.r) {
+        uint32_t x = (uint32_t)(D >> p.shift[y]) & cmask;
+        size_t atv = (((size_t)y * p.F + z) << p.c) | x;
+        rows[y] = reinterpret_cast<const uint4*>(p.active + atv * p.wpa);
+      }
+    }
+    uint32_t nat = 0;
+    for (uint32_t w4 = 0; w4 < p.wpa / 4; ++w4) {
+      uint4 a = __ldcg(rows[0] + w4);
+#pragma unroll
+      for (int y = 1; y < kMaxR; ++y) {
+        if (y < (int)p.r) {
+          uint4 b = __ldcg(rows[y] + w4);
+          a.x &= b.x; a.y &= b.y; a.z &= b.z; a.w &= b.w;
+        }
+      }
+      nat += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+    }
+    double up = 0.0;
+    for (uint32_t y = 0; y < p.r; ++y) {
+      double P = (double)p.aat[y * p.F + z] / p.cells;   // P_{y,z}^{k'}
+      up = (y == 0) ? P : up * P;                          // UP = prod_y P
+    }
+    double est;
+    if (nat == p.g) est = __longlong_as_double(0x7FF0000000000000LL);  // +inf (A20)
+    else est = -(double)p.g * log((double)(p.g - nat) / ((double)p.g * (1.0 - up)));
+    uint32_t flags = (nat == p.g ? 1u : 0u) | (est >= p.theta ? 2u : 0u);
+    const uint32_t ip = p.A_inv * h;                       // f^{-1}
+    ReportDev* R = reinterpret_cast<ReportDev*>(p.reports) + q;
+    R->ip = ip; R->nat = nat; R->estimate = est; R->flags = flags; R->pad = 0;
+    p.keys[q] = ip;
+    p.vals[q] = q;
+    if (flags & 2u) atomicAdd(p.n_above, 1u);
+  }
+}
+
+// gather reports in ascending-ip order (A24)
+__global__ void k_gather(const ReportDev* __restrict__ in, const uint32_t* __restrict__ order,
+                         uint32_t n, ReportDev* __restrict__ out_all) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
+    out_all[q] = in[order[q]];
+}
+
+// --------------------------------------------------------------- export
+
+__global__ void k_export_u8(const uint8_t* __restrict__ in, uint16_t* __restrict__ out, uint64_t n) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
+       q += (uint64_t)gridDim.x * blockDim.x)
+    out[q] = in[q];
+}
+
+__global__ void k_fill_u8(uint8_t* p, uint8_t v, uint64_t n) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
+       q += (uint64_t)gridDim.x * blockDim.x)
+    p[q] = v;
+}
+__global__ void k_fill_u16(uint16_t* p, uint16_t v, uint64_t n) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
+       q += (uint64_t)gridDim.x * blockDim.x)
+    p[q] = v;
+}
+
+// ------------------------------------------------------------ multi-GPU
+
+struct MergeParams {
+  const uint4* touch[kMaxWorld];   // every rank's touch bitmap (peer-mapped)
+  uint4* merged[kMaxWorld];        // every rank's merged bitmap (peer-mapped)
+  uint32_t world;
+  uint64_t lo, hi;                 // this rank's shard of uint4 words
+};
+
+// a5 (A26): OR of every rank's touch words in this rank's shard, stored to every
+// rank's merged bitmap — reduce-scatter and all-gather in one pass over NVLink.
+__global__ void __launch_bounds__(256) k_merge_or(MergeParams p) {
+  for (uint64_t q = p.lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < p.hi;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (uint32_t w = 0; w < p.world; ++w) {
+      uint4 v = __ldcv(p.touch[w] + q);
+      acc.x |= v.x; acc.y |= v.y; acc.z |= v.z; acc.w |= v.w;
+    }
+    for (uint32_t w = 0; w < p.world; ++w) __stcg(p.merged[w] + q, acc);
+  }
+}
+
+struct BarrierParams {
+  uint32_t* pads[kMaxWorld];  // every rank's signal pad (peer-mapped)
+  uint32_t world, rank, epoch;
+};
+
+// Stream-ordered cross-GPU barrier: publish `epoch` into slot [rank] of every
+// peer's pad (release, system scope), then wait until every slot of our pad
+// reached `epoch` (acquire). One process per GPU only (never several ranks on one GPU).
+__global__ void k_barrier(BarrierParams p) {
+  const uint32_t w = threadIdx.x;
+  if (w < p.world) {
+    uint32_t* dst = p.pads[w] + p.rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(dst), "r"(p.epoch) : "memory");
+  }
+  __syncthreads();
+  if (w < p.world) {
+    const uint32_t* src = p.pads[p.rank] + w;
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(src) : "memory");
+    } while ((int32_t)(v - p.epoch) < 0);
+  }
+  __syncthreads();
+}
+
+}  // namespace asse

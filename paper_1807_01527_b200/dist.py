@@ -15,3 +15,44 @@ def shard_slots(n_total, rank, world):
         raise ValueError("bad rank/world")
     n_local = (n_total - rank + world - 1) // world if n_total > rank else 0
     return rank, world, n_local
+
+
+def attach_symmetric_peers(ctx, group=None):
+    """Allocate this rank's touch / merged bitmaps and signal pad in torch symmetric
+    memory (NVLink peer-mapped), exchange the peer pointers and hand them to the
+    library (asse_attach_peers, sync_mode 0: device barrier over the signal pads).
+    Returns the tensors (they must outlive ctx)."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+
+    group = group or dist.group.WORLD
+    dev = torch.device("cuda", torch.cuda.current_device())
+    nbytes = ctx.bitmap_bytes()
+    bufs, ptrs = [], []
+    for size in (nbytes, nbytes, 256):
+        t = symm_mem.empty(size, dtype=torch.uint8, device=dev)
+        t.zero_()
+        h = symm_mem.rendezvous(t, group)
+        bufs.append((t, h))
+        ptrs.append(list(h.buffer_ptrs))
+    torch.cuda.synchronize()
+    dist.barrier(group)
+    ctx.attach_peers(ptrs[0], ptrs[1], ptrs[2], sync_mode=0)
+    return bufs
+
+
+def attach_local_peers(ctxs):
+    """Single-GPU 'virtual ranks' (tests): every context gets plain device buffers
+    and the caller orders the phases (sync_mode 1): scan all ranks, then
+    ctx.merge() for every rank, synchronize, then end_slice for every rank."""
+    import torch
+    nbytes = ctxs[0].bitmap_bytes()
+    touch = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in ctxs]
+    merged = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in ctxs]
+    tp = [t.data_ptr() for t in touch]
+    mp = [t.data_ptr() for t in merged]
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.attach_peers(tp, mp, None, sync_mode=1)
+    return touch, merged

@@ -1,0 +1,165 @@
+"""GPU parity: the sm_100a path through the C-ABI against the CPU oracle, slice by
+slice, on the seeded BASELINE.json traces and on edge cases.
+Pool and CSIP bit-exact, NAT exact, estimates within 1e-6 relative (tests/parity.py)."""
+import numpy as np
+import pytest
+import torch
+
+from gen import PRESETS, Generator
+from oracle import oracle as O
+from paper_1807_01527_b200 import asse
+from parity import compare_pool, compare_reports, step_both, to_device
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(name, **over):
+    p = dict(PRESETS[name], **over)
+    return asse.Asse(**p), O.Oracle(**p), p
+
+
+def test_keys_and_initial_pool(cuda_device):
+    dev, ora, p = _pair("C1")
+    assert dev.keys() == ora.keys()          # both derived from the seed independently (A14)
+    compare_pool(dev.pool(), ora.pool(), "init")
+    assert dev.stats()["code_bytes"] == 1
+    assert dev.stats()["w_theta"] == int(np.ceil(O.w_theta(p["g"], p["theta"])))
+
+
+def test_c1_all_slices(cuda_device):
+    dev, ora, p = _pair("C1")
+    g = Generator("C1")
+    for t in range(p["T"]):
+        rep_d, rep_o = step_both(dev, ora, g.slice(t), p["theta"], "C1 t=%d" % t)
+        assert len(rep_o) > 0 or t == 0
+        # mode 0 (est >= theta) re-read from the same closed slice
+        above = dev.fetch_reports(0)
+        exp = rep_o[(rep_o["flags"] & 2) != 0]
+        compare_reports(above, exp, p["theta"], "C1 mode0 t=%d" % t)
+
+
+def test_c2_all_slices(cuda_device):
+    dev, ora, p = _pair("C2")
+    g = Generator("C2")
+    for t in range(p["T"]):
+        step_both(dev, ora, g.slice(t), p["theta"], "C2 t=%d" % t, check_pool=(t % 3 == 0 or t > 26))
+
+
+@pytest.mark.parametrize("name,N,T", [("C3", 1_000_000, 5), ("C4", 600_000, 4)])
+def test_backbone_geometries_reduced_n(cuda_device, name, N, T):
+    """C3 (u8 codes, k=60) and C4 (u16 codes, k=300, g < 2k so a = 0, A7) geometry."""
+    dev, ora, p = _pair(name)
+    g = Generator(name, N=N)
+    for t in range(T):
+        step_both(dev, ora, g.slice(t), p["theta"], "%s t=%d" % (name, t))
+    if name == "C4":
+        assert dev.stats()["code_bytes"] == 2
+
+
+@pytest.mark.parametrize("name,T", [("C3", 2), ("C4", 2), ("C5", 2)])
+def test_full_size_slices(cuda_device, name, T):
+    """BASELINE.json full per-slice sizes (20M / 10M / 100M packets), the launch
+    configuration bench.py times; full pool and CSIP compared for the first slices."""
+    dev, ora, p = _pair(name)
+    g = Generator(name)
+    for t in range(T):
+        step_both(dev, ora, g.slice(t, threads=16), p["theta"], "%s full t=%d" % (name, t))
+
+
+def test_gpu_generator_matches_host(cuda_device):
+    for name in ("C1", "C2", "C3", "C4"):
+        g = Generator(name)
+        n = 300_000
+        out = torch.empty(2 * n, dtype=torch.int32, device="cuda")
+        g.slice_cuda(2, out.data_ptr(), j0=7, n=n, stride=3)
+        torch.cuda.synchronize()
+        host = g.slice(2, j0=7, n=n, stride=3)
+        assert (out.cpu().numpy().view(np.uint32).reshape(-1, 2) == host).all(), name
+
+
+def test_long_run_sweeps_small_geometry(cuda_device):
+    """k = 300 with g = 128 < 2k (every AT in block 2k-1, swept every k slices,
+    A7): 700 slices cross both sweep points twice; pool parity after every slice."""
+    geo = dict(k=300, r=4, c=8, u=4, s=7, g=128, theta=200.0, seed=42)
+    dev, ora = asse.Asse(**geo), O.Oracle(**geo)
+    rng = np.random.default_rng(3)
+    hosts = rng.integers(0, 2 ** 32, 64).astype(np.uint32)
+    for t in range(700):
+        n = int(rng.integers(0, 3000))
+        pk = np.stack([hosts[rng.integers(0, 64, n)],
+                       rng.integers(0, 2 ** 32, n).astype(np.uint32)], 1).astype(np.uint32)
+        step_both(dev, ora, pk, geo["theta"], "long t=%d" % t, check_pool=(t % 7 == 0 or t in (299, 300, 301, 599, 600, 601)))
+
+
+@pytest.mark.parametrize("k,kp", [(1, 1), (4, 2), (10, 1), (60, 17), (100, 100)])
+def test_window_variants(cuda_device, k, kp):
+    """discrete window k = 1, k' < k (Alg. 1), and u16 codes at k = 100."""
+    geo = dict(k=k, k_prime=kp, r=4, c=10, u=4, s=6, g=256, theta=300.0, seed=9)
+    dev, ora = asse.Asse(**geo), O.Oracle(**geo)
+    g = Generator("C2", N=150_000)
+    for t in range(min(2 * k + 3, 14)):
+        step_both(dev, ora, g.slice(t), geo["theta"], "k=%d k'=%d t=%d" % (k, kp, t))
+
+
+def test_edge_cases_empty_ragged_misaligned_split(cuda_device):
+    dev, ora, p = _pair("C1")
+    g = Generator("C1")
+    # empty slice
+    step_both(dev, ora, np.zeros((0, 2), np.uint32), p["theta"], "empty")
+    # one packet, then odd counts, a misaligned buffer and several scan calls per slice
+    step_both(dev, ora, g.slice(0, n=1), p["theta"], "n=1")
+    step_both(dev, ora, g.slice(1, n=12345), p["theta"], "odd", offset=1)
+    step_both(dev, ora, g.slice(2), p["theta"], "split", split=7)
+    step_both(dev, ora, g.slice(3, n=99999), p["theta"], "split+misaligned", split=3, offset=1)
+
+
+def test_order_invariance_and_host_ingest(cuda_device):
+    """concurrent SetATs are order independent; the host-buffer entry point
+    (double-buffered H2D) gives the identical state."""
+    p = dict(PRESETS["C2"])
+    a, b, c = asse.Asse(**p), asse.Asse(**p), asse.Asse(**p)
+    g = Generator("C2")
+    rng = np.random.default_rng(0)
+    for t in range(3):
+        pk = g.slice(t)
+        d1, _ = to_device(pk)
+        d2, _ = to_device(pk[rng.permutation(len(pk))])
+        a.scan_slice(d1)
+        b.scan_slice(d2)
+        c.scan_slice_host(np.ascontiguousarray(pk))
+        ra, rb, rc = a.end_slice(), b.end_slice(), c.end_slice()
+        assert (ra == rb).all() and (ra == rc).all()
+        pa = a.pool()
+        assert (pa == b.pool()).all() and (pa == c.pool()).all()
+
+
+def test_overflow_reported_and_state_continues(cuda_device):
+    geo = dict(PRESETS["C1"], max_candidates=50)
+    dev, ora = asse.Asse(**geo), O.Oracle(**geo)
+    g = Generator("C1")
+    for t in range(4):
+        pk = g.slice(t)
+        d, ptr = to_device(pk)
+        dev.scan_slice(ptr, len(pk))
+        ora.scan(pk)
+        st_o = ora.detect()
+        ora.advance()
+        try:
+            dev.end_slice()
+            st_d = 0
+        except asse.AsseError as e:
+            st_d = e.status
+        assert (st_d == asse.E_OVERFLOW) == (st_o == -4), t
+        compare_pool(dev.pool(), ora.pool(), "overflow t=%d" % t)
+
+
+def test_state_machine_errors(cuda_device):
+    geo = dict(PRESETS["C1"], n_slices=2)
+    dev = asse.Asse(**geo)
+    dev.end_slice()
+    dev.end_slice()
+    with pytest.raises(asse.AsseError) as e:
+        dev.end_slice()
+    assert e.value.status == asse.E_STATE
+    with pytest.raises(asse.AsseError):
+        asse.Asse(**dict(PRESETS["C1"], g=100))
