@@ -77,6 +77,7 @@ class Generator:
         """Host packets of slice t: uint32 array shape (n, 2) = [aip, bip] per slot."""
         if n is None:
             n = (self.N - j0 + stride - 1) // stride
+        self._check(j0, n, stride)
         out = np.empty((n, 2), dtype=np.uint32)
         lib().gen_fill(self._h, t, j0, stride, n, out.ctypes.data, threads)
         return out
@@ -85,10 +86,15 @@ class Generator:
         """Fill n packets (slots j0 + m*stride) into device memory at out_ptr."""
         if n is None:
             n = (self.N - j0 + stride - 1) // stride
+        self._check(j0, n, stride)
         rc = lib().gen_cuda_fill(self._h, t, j0, stride, n, out_ptr, stream)
         if rc != 0:
             raise RuntimeError("gen_cuda_fill failed")
         return n
+
+    def _check(self, j0, n, stride):
+        if n and (j0 + (n - 1) * stride >= self.N or stride < 1):
+            raise ValueError("slots j0 + m*stride must stay below N=%d" % self.N)
 
     # metadata for accuracy / planted checks
     def planted(self):

@@ -153,7 +153,6 @@ template <> struct Swar<1> {
   static constexpr int EPW = 4;     // elements per word
   static constexpr int EB = 8;      // element bits
   static constexpr uint32_t G = 0x80808080u;
-  static constexpr uint32_t SIGN = 0xBA98u;  // PRMT: replicate the msb of every byte
   static constexpr uint32_t EMPTY_LO = 127u;
 };
 template <> struct Swar<2> {
@@ -161,7 +160,6 @@ template <> struct Swar<2> {
   static constexpr int EPW = 2;
   static constexpr int EB = 16;
   static constexpr uint32_t G = 0x80008000u;
-  static constexpr uint32_t SIGN = 0xBB99u;  // replicate the msb of each half-word
   static constexpr uint32_t EMPTY_LO = 32767u;
 };
 
@@ -185,6 +183,7 @@ __global__ void __launch_bounds__(256) k_fold(FoldParams p) {
   using S = Swar<CB>;
   constexpr int NW = S::NW, EPW = S::EPW, EB = S::EB;
   constexpr uint32_t G = S::G;
+  constexpr uint32_t EMASK = (EB == 8) ? 0xFFu : 0xFFFFu;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lpa = 1u << p.lpa_log2;            // lanes per ATV (8, 16, 32)
   const uint32_t lia = lane & (lpa - 1u);           // lane within its ATV
@@ -283,7 +282,7 @@ __global__ void __launch_bounds__(256) k_fold(FoldParams p) {
       // preserveAT for slice t+1 (Alg. 2), only in words holding swept blocks
       if (swept_mask & (1u << q)) {
         uint32_t er = (in_range(vx, x, LE1[q], HE1[q]) | in_range(vx, x, LE2[q], HE2[q])) & G;
-        uint32_t m = __byte_perm(er, 0u, S::SIGN);
+        uint32_t m = (er >> (EB - 1)) * EMASK;   // guard bit -> whole-element mask
         x = (x & ~m) | (TWOK & m);
       }
       changed |= (x != cur[q]);

@@ -18,6 +18,8 @@ def test_deterministic_and_shardable():
             s = g.slice(3, j0=rank, stride=D, n=5000)
             assert (s == a[rank::D][:5000]).all()
         assert not (g.slice(4, n=1000) == a[:1000]).all()
+        with pytest.raises(ValueError):
+            g.slice(0, j0=g.N - 1, n=2)
 
 
 def test_c1_shape():
