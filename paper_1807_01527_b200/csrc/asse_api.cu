@@ -40,6 +40,7 @@ struct Ctx {
   uint64_t t = 0;
   // device
   int device = 0, sms = 148;
+  int scan_grid = 0, fold_grid = 0;   // resident CTAs (SMs x occupancy)
   cudaStream_t stream = nullptr, copy_stream = nullptr;
   void* pool = nullptr;
   uint32_t* touch_own = nullptr;
@@ -122,7 +123,7 @@ static asse_status validate(const asse_config* cfg, std::string* why) {
   if (p.k > 16383) return bad("k <= 16383 (15-bit device codes)");
   if (p.r < 2 || p.r > (uint32_t)kMaxR) return bad("2 <= r <= 8");
   if (p.c < 2 || p.u > 16 || p.c + p.u > 32) return bad("c >= 2, u <= 16, c + u <= 32");
-  if (p.c > 24) return bad("c <= 24");
+  if (p.c + p.u > 24) return bad("device path: c + u <= 24 (32-bit ATV indices)");
   if (p.s < 1 || p.s > p.c) return bad("1 <= s <= c");
   if (!(p.theta > 0)) return bad("theta > 0");
   if (p.g < 128 || p.g > 512 || (p.g & (p.g - 1))) return bad("device path: g in {128, 256, 512}");
@@ -165,6 +166,24 @@ static void free_all(Ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
+template <int CB, int LPAL>
+static cudaError_t fold_occ_t(int* occ) {
+  cudaError_t e = cudaFuncSetAttribute(k_fold<CB, LPAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)fold_smem<CB>());
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_fold<CB, LPAL>, kFoldThreads, fold_smem<CB>());
+}
+static cudaError_t fold_occupancy(uint32_t cb, uint32_t lpal, int* occ) {
+  if (cb == 1) return lpal == 3 ? fold_occ_t<1, 3>(occ) : lpal == 4 ? fold_occ_t<1, 4>(occ) : fold_occ_t<1, 5>(occ);
+  return lpal == 3 ? fold_occ_t<2, 3>(occ) : lpal == 4 ? fold_occ_t<2, 4>(occ) : fold_occ_t<2, 5>(occ);
+}
+template <int CB>
+static void launch_fold(uint32_t lpal, unsigned blocks, cudaStream_t s, const FoldParams& fp) {
+  if (lpal == 3) k_fold<CB, 3><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
+  else if (lpal == 4) k_fold<CB, 4><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
+  else k_fold<CB, 5><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
+}
+
 static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cudaStream_t st) {
   if (n == 0) return ASSE_OK;
   ScanParams p{};
@@ -176,10 +195,8 @@ static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cuda
   p.cmask = (1u << c->cfg.c) - 1u;
   p.wpa = c->wpa;
   for (int y = 0; y < kMaxR; ++y) p.shift[y] = c->shift[y];
-  uint64_t bodies = n / 2 + 1;
-  uint64_t blocks = (bodies + 255) / 256;
-  uint64_t maxb = (uint64_t)c->sms * 8;
-  if (blocks > maxb) blocks = maxb;
+  const uint64_t tiles = ((n / 2) * 16 + kScanTileBytes - 1) / kScanTileBytes;
+  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)c->scan_grid));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing) {
     if (c->ev_free.size() < 2) {
@@ -194,9 +211,9 @@ static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cuda
     CK(cudaEventRecord(e0, st));
   }
   if (c->cb == 1)
-    k_scan<1><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const uint2*>(d_pairs), n, p);
+    k_scan<1><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(reinterpret_cast<const uint2*>(d_pairs), n, p);
   else
-    k_scan<2><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const uint2*>(d_pairs), n, p);
+    k_scan<2><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(reinterpret_cast<const uint2*>(d_pairs), n, p);
   CK(cudaGetLastError());
   LAUNCHED(c);
   c->stats.scan_launches++;
@@ -321,6 +338,19 @@ asse_status asse_init(const asse_config* cfg, void** out) {
   CKI(cudaSetDevice(c->device));
   CKI(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
   CKI(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  {
+    int occ = 0;
+    if (c->cb == 1) {
+      CKI(cudaFuncSetAttribute(k_scan<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem));
+      CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<1>, kScanThreads, kScanSmem));
+    } else {
+      CKI(cudaFuncSetAttribute(k_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem));
+      CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<2>, kScanThreads, kScanSmem));
+    }
+    c->scan_grid = std::max(1, occ) * c->sms;
+    CKI(fold_occupancy(c->cb, c->lpa_log2, &occ));
+    c->fold_grid = std::max(1, occ) * c->sms;
+  }
   CKI(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   const uint64_t bm_bytes = c->n_atv * c->wpa * 4;
   CKI(cudaMalloc(&c->pool, c->n_at * c->cb));
@@ -539,10 +569,11 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
     fp.n_chunks = c->n_at / 512;
     fp.g = p.g; fp.k = p.k; fp.kp = c->kp; fp.C0 = c->C0; fp.a = c->a;
     fp.c = p.c; fp.w_theta = c->w_theta; fp.lpa_log2 = c->lpa_log2;
-    uint64_t blocks = std::min<uint64_t>((fp.n_chunks + 7) / 8, (uint64_t)c->sms * 4);
+    const uint64_t tiles = (fp.n_chunks + kFoldChunksPerTile - 1) / kFoldChunksPerTile;
+    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)c->fold_grid));
     if (c->timing) CK(cudaEventRecord(c->ev[2], s));
-    if (c->cb == 1) k_fold<1><<<(unsigned)blocks, 256, 0, s>>>(fp);
-    else k_fold<2><<<(unsigned)blocks, 256, 0, s>>>(fp);
+    if (c->cb == 1) launch_fold<1>(c->lpa_log2, (unsigned)blocks, s, fp);
+    else launch_fold<2>(c->lpa_log2, (unsigned)blocks, s, fp);
     CK(cudaGetLastError());
     LAUNCHED(c);
     c->stats.fold_launches++;

@@ -13,12 +13,16 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "asse_tma.cuh"
+
 namespace asse {
 
 constexpr int kMaxR = 8;       // rows supported by the device path
 constexpr int kMaxWorld = 16;  // ranks supported by the peer merge
 
 // ------------------------------------------------------------------ helpers
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ uint32_t bh_index(uint32_t bip, uint64_t kbh, uint32_t g) {
   // BH (A13): SplitMix64 finalizer of bip ^ K_bh, multiply-shift to [0, g)
@@ -42,6 +46,11 @@ __device__ __forceinline__ uint32_t touch_bit(uint32_t i) {
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
 // streaming read-only input (packets): no L1 allocation, evict-first in L2
@@ -97,33 +106,68 @@ __device__ __forceinline__ void scan_pair(const ScanParams& p, uint32_t aip, uin
   }
 }
 
+constexpr int kScanConsumerWarps = 8;
+constexpr int kScanThreads = 32 * (kScanConsumerWarps + 1);   // + 1 producer warp
+constexpr uint32_t kScanTileBytes = 16384;                      // 2048 packets per stage
+constexpr int kScanStages = 4;
+constexpr size_t kScanSmem = (size_t)kScanStages * kScanTileBytes;
+
+// Alg. 3 over a device packet buffer. The 16-B aligned body is streamed through a
+// 4-stage shared-memory ring by bulk copies (TMA, cp.async.bulk; one producer warp),
+// tile i of this CTA = body tile blockIdx.x + i*gridDim.x; the 8 consumer warps
+// hash the packets and issue r RED.OR per packet into the L2-resident touch bitmap.
 template <int CB>
-__global__ void __launch_bounds__(256) k_scan(const uint2* __restrict__ pk, uint64_t n,
-                                              ScanParams p) {
-  // head / tail packets when the buffer is not 16-byte aligned or n is odd
+__global__ void __launch_bounds__(kScanThreads) k_scan(const uint2* __restrict__ pk, uint64_t n,
+                                                       ScanParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[kScanStages], empty[kScanStages];
   const uint32_t head = (((uintptr_t)pk) & 15u) ? 1u : 0u;
-  const uint64_t nb = (n > head) ? (n - head) >> 1 : 0;  // uint4 bodies (2 packets each)
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
-  if (tid == 0) {
+  const uint64_t nbody = (n > head) ? n - head : 0;
+  const uint64_t body_bytes = (nbody >> 1) * 16u;
+  const uint64_t n_tiles = (body_bytes + kScanTileBytes - 1) / kScanTileBytes;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {     // scalar head / odd tail packets
     if (head && n > 0) scan_pair<CB>(p, pk[0].x, pk[0].y);
-    if (n > head && ((n - head) & 1)) scan_pair<CB>(p, pk[n - 1].x, pk[n - 1].y);
+    if (nbody & 1) scan_pair<CB>(p, pk[n - 1].x, pk[n - 1].y);
   }
-  const uint4* body = reinterpret_cast<const uint4*>(pk + head);
-  const uint64_t pol = policy_evict_first();
-  uint64_t q = tid;
-  for (; q + nthr < nb; q += 2 * nthr) {
-    uint4 v0 = ld_stream(body + q, pol);
-    uint4 v1 = ld_stream(body + q + nthr, pol);
-    scan_pair<CB>(p, v0.x, v0.y);
-    scan_pair<CB>(p, v0.z, v0.w);
-    scan_pair<CB>(p, v1.x, v1.y);
-    scan_pair<CB>(p, v1.z, v1.w);
+  const uint64_t my_tiles =
+      (n_tiles > blockIdx.x) ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kScanStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kScanConsumerWarps);
+    }
+    mbar_fence_init();
   }
-  if (q < nb) {
-    uint4 v0 = ld_stream(body + q, pol);
-    scan_pair<CB>(p, v0.x, v0.y);
-    scan_pair<CB>(p, v0.z, v0.w);
+  __syncthreads();
+  const uint8_t* body = reinterpret_cast<const uint8_t*>(pk + head);
+  if (warp == kScanConsumerWarps) {              // producer warp
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (uint64_t i = 0; i < my_tiles; ++i) {
+        const uint32_t st = (uint32_t)(i % kScanStages);
+        if (i >= kScanStages) mbar_wait(&empty[st], (uint32_t)((i / kScanStages) - 1) & 1u);
+        const uint64_t off = (blockIdx.x + i * gridDim.x) * (uint64_t)kScanTileBytes;
+        const uint32_t bytes = (uint32_t)umin64(kScanTileBytes, body_bytes - off);
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(smem + (size_t)st * kScanTileBytes, body + off, bytes, &full[st], pol);
+      }
+    }
+    return;
+  }
+  for (uint64_t i = 0; i < my_tiles; ++i) {
+    const uint32_t st = (uint32_t)(i % kScanStages);
+    mbar_wait(&full[st], (uint32_t)(i / kScanStages) & 1u);
+    const uint64_t off = (blockIdx.x + i * gridDim.x) * (uint64_t)kScanTileBytes;
+    const uint32_t n4 = (uint32_t)umin64(kScanTileBytes, body_bytes - off) >> 4;
+    const uint4* tp = reinterpret_cast<const uint4*>(smem + (size_t)st * kScanTileBytes);
+    for (uint32_t q = threadIdx.x; q < n4; q += 32 * kScanConsumerWarps) {
+      const uint4 v = tp[q];
+      scan_pair<CB>(p, v.x, v.y);
+      scan_pair<CB>(p, v.z, v.w);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
 }
 
@@ -178,18 +222,64 @@ __device__ __forceinline__ uint32_t in_range(uint32_t vx, uint32_t v, uint32_t L
 //   preserveAT  for slice t+1 on ATs whose block ACT becomes 0 or k  (Alg. 2)
 // The per-AT constants depend only on the AT index, so each lane computes them
 // once per launch and keeps them in registers (blocked warp -> chunk mapping).
-template <int CB>
-__global__ void __launch_bounds__(256) k_fold(FoldParams p) {
+constexpr int kFoldConsumerWarps = 8;
+constexpr int kFoldThreads = 32 * (kFoldConsumerWarps + 1);   // + 1 producer warp
+constexpr uint32_t kFoldChunksPerTile = 16;                    // 16 x 512 ATs per stage
+constexpr int kFoldStages = 4;
+template <int CB> constexpr uint32_t fold_code_bytes() { return kFoldChunksPerTile * 512u * CB; }
+template <int CB> constexpr uint32_t fold_stage_bytes() { return fold_code_bytes<CB>() + kFoldChunksPerTile * 64u; }
+template <int CB> constexpr size_t fold_smem() { return (size_t)kFoldStages * fold_stage_bytes<CB>(); }
+
+template <int CB, int LPAL>   // LPAL = log2(lanes per ATV) = log2(g/16): 3, 4 or 5
+__global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
   using S = Swar<CB>;
   constexpr int NW = S::NW, EPW = S::EPW, EB = S::EB;
   constexpr uint32_t G = S::G;
   constexpr uint32_t EMASK = (EB == 8) ? 0xFFu : 0xFFFFu;
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t lpa = 1u << p.lpa_log2;            // lanes per ATV (8, 16, 32)
-  const uint32_t lia = lane & (lpa - 1u);           // lane within its ATV
+  constexpr uint32_t CODE_BYTES = fold_code_bytes<CB>();
+  constexpr uint32_t STAGE_BYTES = fold_stage_bytes<CB>();
+  constexpr uint32_t LPA = 1u << LPAL;
+  constexpr uint32_t FIELD = 1u << (LPAL);        // bits per packed ATV weight: 8, 16, 32
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[kFoldStages], empty[kFoldStages];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  // blocked tile range of this CTA (keeps each warp's (y, z) slab changes rare for AAT)
+  const uint32_t n_tiles = (uint32_t)((p.n_chunks + kFoldChunksPerTile - 1) / kFoldChunksPerTile);
+  const uint32_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const uint32_t t0 = blockIdx.x * per;
+  const uint32_t t1 = min(n_tiles, t0 + per);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kFoldStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kFoldConsumerWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (t0 >= t1) return;
+  if (warp == kFoldConsumerWarps) {                 // producer warp: TMA bulk loads
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const uint64_t keep = policy_evict_last();
+      for (uint32_t i = 0; i < t1 - t0; ++i) {
+        const uint32_t st = i % kFoldStages;
+        if (i >= kFoldStages) mbar_wait(&empty[st], ((i / kFoldStages) - 1) & 1u);
+        const uint32_t tile = t0 + i;
+        const uint32_t nch = (uint32_t)umin64(kFoldChunksPerTile, p.n_chunks - (uint64_t)tile * kFoldChunksPerTile);
+        uint8_t* dst = smem + (size_t)st * STAGE_BYTES;
+        mbar_expect_tx(&full[st], nch * (512u * CB + 64u));
+        bulk_g2s(dst, reinterpret_cast<const uint8_t*>(p.pool) + (size_t)tile * CODE_BYTES, nch * 512u * CB,
+                 &full[st], pol);
+        bulk_g2s(dst + CODE_BYTES, p.touch_src + (size_t)tile * kFoldChunksPerTile * 16u, nch * 64u,
+                 &full[st], keep);
+      }
+    }
+    return;
+  }
+  const uint32_t lia = lane & (LPA - 1u);           // lane within its ATV
   const uint32_t two_k = 2u * p.k;
 
-  // ---- per-lane, per-element constants (positions i = 16*lia + e)
+  // ---- per-lane, per-element constants (positions i = 16*lia + e), computed once
   uint32_t CLK[NW], LO1[NW], HI1[NW], LO2[NW], HI2[NW], LE1[NW], HE1[NW], LE2[NW], HE2[NW];
   uint32_t swept_mask = 0;  // bit q: word q holds ATs of a block swept for t+1
 #pragma unroll
@@ -206,8 +296,8 @@ __global__ void __launch_bounds__(256) k_fold(FoldParams p) {
       // Alg. 2 for the new ACT of slice t+1
       uint32_t nclk = (clk + 1u == two_k) ? 0u : clk + 1u;
       uint32_t le1 = S::EMPTY_LO, he1 = 0, le2 = S::EMPTY_LO, he2 = 0;
-      if (nclk == 0) { le1 = 0; he1 = p.k; }                         // 0 <= at <= k
-      else if (nclk == p.k) { le1 = p.k; he1 = two_k - 1u; le2 = 0; he2 = 0; }  // k..2k-1, 0
+      if (nclk == 0) { le1 = 0; he1 = p.k; }                                   // 0 <= at <= k
+      else if (nclk == p.k) { le1 = p.k; he1 = two_k - 1u; le2 = 0; he2 = 0; } // k..2k-1 and 0
       if (le1 <= he1 || le2 <= he2) swept_mask |= 1u << q;
       const uint32_t sh = (uint32_t)e * EB;
       const uint32_t gbit = 1u << (EB - 1);
@@ -218,113 +308,107 @@ __global__ void __launch_bounds__(256) k_fold(FoldParams p) {
       LE2[q] |= le2 << sh; HE2[q] |= (he2 | gbit) << sh;
     }
   }
-  // warp-uniform: words that need the erase step in any lane
-  swept_mask = __reduce_or_sync(0xFFFFFFFFu, swept_mask);
+  swept_mask = __reduce_or_sync(0xFFFFFFFFu, swept_mask);   // warp-uniform per word
   uint32_t TWOK = 0;
 #pragma unroll
   for (int e = 0; e < EPW; ++e) TWOK |= two_k << (e * EB);
 
-  // ---- blocked chunk range of this warp
-  const uint64_t warp_global = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t per = (p.n_chunks + n_warps - 1) / n_warps;
-  const uint64_t c0 = warp_global * per;
-  const uint64_t c1 = min(p.n_chunks, c0 + per);
-  if (c0 >= c1) return;
-
-  constexpr int LANE_WORDS = NW;  // uint32 words of codes per lane
+  constexpr int LW = NW;                            // uint32 code words per lane
   const uint64_t pol = policy_evict_first();
-  uint4* pool4 = reinterpret_cast<uint4*>(p.pool);
   const uint32_t tshift = (lane & 1u) << 4;
-  const uint32_t atvs_per_chunk_log2 = 5u - p.lpa_log2;
+  const uint32_t fshift = (lane >> LPAL) * FIELD;   // this lane's ATV field in the packed sum
   const uint32_t E = 1u << p.c;
-
-  uint32_t cur[LANE_WORDS], nxt[LANE_WORDS];
-  uint32_t tw_cur, tw_nxt = 0;
-  auto load = [&](uint64_t ch, uint32_t* dst, uint32_t& tw) {
-    const uint4* src = pool4 + (ch * 32u + lane) * (LANE_WORDS / 4);
-#pragma unroll
-    for (int v = 0; v < LANE_WORDS / 4; ++v) {
-      uint4 t4 = ld_pool(src + v, pol);
-      dst[4 * v + 0] = t4.x; dst[4 * v + 1] = t4.y; dst[4 * v + 2] = t4.z; dst[4 * v + 3] = t4.w;
-    }
-    tw = __ldcg(p.touch_src + ch * 16u + (lane >> 1));
-  };
-  load(c0, cur, tw_cur);
-
+  uint4* const gpool = reinterpret_cast<uint4*>(p.pool) + lane * (LW / 4);
+  uint32_t* const gact = p.active + (lane >> 1);
+  uint32_t* const gzero = p.touch_zero + (lane >> 1);
   unsigned long long aat_acc = 0;
   uint32_t aat_yz = 0xFFFFFFFFu;
   uint32_t nsup = 0;
 
-  for (uint64_t ch = c0; ch < c1; ++ch) {
-    if (ch + 1 < c1) load(ch + 1, nxt, tw_nxt);
-    const uint32_t field = (tw_cur >> tshift) & 0xFFFFu;
-    uint32_t v[LANE_WORDS];
-    uint32_t cnt = 0, accbits = 0;
-    bool changed = false;
+  for (uint32_t i = 0; i < t1 - t0; ++i) {
+    const uint32_t st = i % kFoldStages;
+    mbar_wait(&full[st], (i / kFoldStages) & 1u);
+    const uint32_t tile = t0 + i;
+    const uint32_t nch = (uint32_t)umin64(kFoldChunksPerTile, p.n_chunks - (uint64_t)tile * kFoldChunksPerTile);
+    const uint8_t* sbase = smem + (size_t)st * STAGE_BYTES;
+    const uint4* scodes = reinterpret_cast<const uint4*>(sbase) + lane * (LW / 4);
+    const uint32_t* stouch = reinterpret_cast<const uint32_t*>(sbase + CODE_BYTES) + (lane >> 1);
+    for (uint32_t cc = warp; cc < nch; cc += kFoldConsumerWarps) {
+      const uint32_t ch = tile * kFoldChunksPerTile + cc;
+      uint32_t cur[LW];
 #pragma unroll
-    for (int q = 0; q < NW; ++q) {
-      // SetAT fold via PRMT: element e takes byte(s) of CLK when its touch bit is set
-      uint32_t sel;
-      if (CB == 1) {
-        uint32_t f = (q <= 2) ? (field << (2 - q)) : (field >> (q - 2));
-        sel = 0x3210u | (f & 0x4444u);
-      } else {
-        sel = 0x3210u | (((field >> q) & 0x0101u) * 0x44u);
+      for (int v4 = 0; v4 < LW / 4; ++v4) {
+        const uint4 t4 = scodes[cc * (32u * LW / 4) + v4];
+        cur[4 * v4 + 0] = t4.x; cur[4 * v4 + 1] = t4.y; cur[4 * v4 + 2] = t4.z; cur[4 * v4 + 3] = t4.w;
       }
-      uint32_t x = __byte_perm(cur[q], CLK[q], sel);
-      // checkAT (Alg. 1): two intervals of the cyclic window
-      uint32_t vx = x | G;
-      uint32_t act = (in_range(vx, x, LO1[q], HI1[q]) | in_range(vx, x, LO2[q], HI2[q])) & G;
-      cnt += __popc(act);
-      if (CB == 1) accbits |= act >> (7 - q);
-      else accbits |= act >> (15 - q);
-      // preserveAT for slice t+1 (Alg. 2), only in words holding swept blocks
-      if (swept_mask & (1u << q)) {
-        uint32_t er = (in_range(vx, x, LE1[q], HE1[q]) | in_range(vx, x, LE2[q], HE2[q])) & G;
-        uint32_t m = (er >> (EB - 1)) * EMASK;   // guard bit -> whole-element mask
-        x = (x & ~m) | (TWOK & m);
+      const uint32_t field = (stouch[cc * 16u] >> tshift) & 0xFFFFu;
+      uint32_t v[LW];
+      uint32_t cnt = 0, accbits = 0;
+      bool changed = false;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        // SetAT fold via PRMT: element e takes CLK's element when its touch bit is set
+        uint32_t sel;
+        if (CB == 1) {
+          const uint32_t f = (q <= 2) ? (field << (2 - q)) : (field >> (q - 2));
+          sel = 0x3210u | (f & 0x4444u);
+        } else {
+          sel = 0x3210u | (((field >> q) & 0x0101u) * 0x44u);
+        }
+        uint32_t x = __byte_perm(cur[q], CLK[q], sel);
+        // checkAT (Alg. 1): two intervals of the cyclic window
+        const uint32_t vx = x | G;
+        const uint32_t act = (in_range(vx, x, LO1[q], HI1[q]) | in_range(vx, x, LO2[q], HI2[q])) & G;
+        cnt += __popc(act);
+        accbits |= act >> ((CB == 1 ? 7 : 15) - q);
+        // preserveAT for slice t+1 (Alg. 2), only in words holding swept blocks
+        if (swept_mask & (1u << q)) {
+          const uint32_t er = (in_range(vx, x, LE1[q], HE1[q]) | in_range(vx, x, LE2[q], HE2[q])) & G;
+          const uint32_t m = (er >> (EB - 1)) * EMASK;   // guard bit -> whole-element mask
+          x = (x & ~m) | (TWOK & m);
+        }
+        changed |= (x != cur[q]);
+        v[q] = x;
       }
-      changed |= (x != cur[q]);
-      v[q] = x;
-    }
-    // write back only the 16/32-byte lane slices that changed
-    if (changed) {
-      uint4* dst = pool4 + (ch * 32u + lane) * (LANE_WORDS / 4);
+      if (changed) {   // write back only the lane slices that changed
 #pragma unroll
-      for (int w4 = 0; w4 < LANE_WORDS / 4; ++w4)
-        st_pool(dst + w4, make_uint4(v[4 * w4], v[4 * w4 + 1], v[4 * w4 + 2], v[4 * w4 + 3]), pol);
+        for (int w4 = 0; w4 < LW / 4; ++w4)
+          st_pool(gpool + (size_t)ch * (32u * LW / 4) + w4,
+                  make_uint4(v[4 * w4], v[4 * w4 + 1], v[4 * w4 + 2], v[4 * w4 + 3]), pol);
+      }
+      // active word = even-lane bits | odd-lane bits shifted into the free positions
+      const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, accbits, 1);
+      if ((lane & 1u) == 0) {
+        gact[(size_t)ch * 16u] = (CB == 1) ? (accbits | (other << 4)) : (accbits | (other << 8));
+        gzero[(size_t)ch * 16u] = 0u;
+      }
+      // |ATV|^{k'} of every ATV in the chunk with one warp reduction: each ATV's
+      // lanes add into their own FIELD-bit slot (max 16*LPA fits the slot)
+      const uint32_t packed = __reduce_add_sync(0xFFFFFFFFu, cnt << fshift);
+      const uint32_t w = (FIELD == 32) ? packed : ((packed >> fshift) & ((1u << FIELD) - 1u));
+      uint32_t tot;
+      if (LPAL == 5) tot = packed;
+      else if (LPAL == 4) tot = (packed & 0xFFFFu) + (packed >> 16);
+      else tot = (packed & 0xFFu) + ((packed >> 8) & 0xFFu) + ((packed >> 16) & 0xFFu) + (packed >> 24);
+      const uint32_t atv = (ch << (5 - LPAL)) + (lane >> LPAL);
+      const uint32_t yz = atv >> p.c;
+      if (lia == 0 && w >= p.w_theta) {            // super ATV
+        const uint32_t xcol = atv & (E - 1u);
+        const uint32_t slot = atomicAdd(p.sa_cnt + yz, 1u);
+        p.sa_list[(size_t)yz * E + slot] = xcol;
+        atomicOr(p.sa_bits + (atv >> 5), 1u << (xcol & 31u));
+        nsup++;
+      }
+      // AAT: the whole chunk lies in one (y, z) slab (E*g >= 512)
+      if (yz != aat_yz) {
+        if (lane == 0 && aat_acc) atomicAdd(p.aat + aat_yz, aat_acc);
+        aat_yz = yz;
+        aat_acc = 0;
+      }
+      aat_acc += tot;
     }
-    // active word = even lane bits | odd lane bits shifted into the free positions
-    uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, accbits, 1);
-    if ((lane & 1u) == 0) {
-      uint32_t word = (CB == 1) ? (accbits | (other << 4)) : (accbits | (other << 8));
-      p.active[ch * 16u + (lane >> 1)] = word;
-      p.touch_zero[ch * 16u + (lane >> 1)] = 0u;
-    }
-    // weight of each ATV in the chunk: reduce over its lpa lanes
-    uint32_t w = cnt;
-    for (uint32_t off = lpa >> 1; off > 0; off >>= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, off);
-    const uint64_t atv = (ch << atvs_per_chunk_log2) + (lane >> p.lpa_log2);
-    const uint32_t yz = (uint32_t)(atv >> p.c);
-    const uint32_t xcol = (uint32_t)atv & (E - 1u);
-    if (lia == 0 && w >= p.w_theta) {            // super ATV
-      uint32_t slot = atomicAdd(p.sa_cnt + yz, 1u);
-      p.sa_list[(size_t)yz * E + slot] = xcol;
-      atomicOr(p.sa_bits + (((size_t)yz * E + xcol) >> 5), 1u << (xcol & 31u));
-      nsup++;
-    }
-    // AAT: the whole chunk lies in one (y, z) slab (E*g >= 512)
-    uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, cnt);
-    if (yz != aat_yz) {
-      if (aat_yz != 0xFFFFFFFFu && lane == 0 && aat_acc) atomicAdd(p.aat + aat_yz, aat_acc);
-      aat_yz = yz;
-      aat_acc = 0;
-    }
-    aat_acc += tot;
-#pragma unroll
-    for (int q = 0; q < LANE_WORDS; ++q) cur[q] = nxt[q];
-    tw_cur = tw_nxt;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
   if (lane == 0 && aat_acc) atomicAdd(p.aat + aat_yz, aat_acc);
   nsup = __reduce_add_sync(0xFFFFFFFFu, nsup);
