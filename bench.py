@@ -239,11 +239,15 @@ def main():
     with ClockSampler(local) as clk:
         ev0.record(stream)
         n_rep = 0
+        phases = {k: [] for k in ("last_merge_ms", "last_fold_ms", "last_restore_ms", "last_nat_ms",
+                                  "last_sort_ms")}
         for t in range(args.warmup, args.warmup + args.steps):
             rep = step(t)
             n_rep += len(rep)
             s = ctx.stats()
             end_ms.append(s["last_end_slice_ms"])
+            for k in phases:
+                phases[k].append(s[k])
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -312,6 +316,7 @@ def main():
                        "l2": "inputs larger than L2 (%d MB per slice per GPU), no flush" % (8 * n_local >> 20)},
             "end_slice_ms": statistics.mean(end_ms),
             "end_slice_ms_max": max(end_ms),
+            "end_slice_breakdown_ms": {k[5:-3]: statistics.mean(v) for k, v in phases.items()},
             "clocks": clk.summary(),
             "e2e": e2e,
             "gpu_launches": launches,

@@ -51,7 +51,14 @@ struct Ctx {
   uint32_t* sa_cnt = nullptr;
   uint32_t* sa_list = nullptr;
   uint32_t* sa_bits = nullptr;
-  uint32_t* counters = nullptr;     // [0] n_cand [1] overflow [2] n_above [3] n_super [4] n_sel
+  uint32_t* counters = nullptr;     // [0] n_cand [1] overflow [2] n_above [3] n_super [4] n_sel [5] big
+  void* scratch = nullptr;          // aat | sa_cnt | counters | sa_bits, zeroed per slice
+  size_t scratch_bytes = 0;
+  RestoreParams rp0{};              // geometry part of the restore parameters
+  uint32_t* d_clock = nullptr;      // device copy of C0, refreshed from h_clock per slice
+  uint32_t* h_clock = nullptr;      // pinned
+  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [timing][mode]
+  size_t restore_smem = 0;
   uint32_t* ws = nullptr;
   uint64_t ws_cap = 0;
   uint32_t* cand = nullptr;
@@ -64,8 +71,10 @@ struct Ctx {
   uint16_t* export_buf = nullptr;
   // host pinned
   uint32_t* h_counters = nullptr;
-  ReportDev* h_rep = nullptr;
+  ReportDev* h_rep = nullptr;       // fixed prefix buffer (a CUDA-graph copy target)
   uint64_t h_rep_cap = 0;
+  ReportDev* h_big = nullptr;       // larger report copies
+  uint64_t h_big_cap = 0;
   // host-buffer scan staging (P:428 double buffering)
   uint32_t* stage[2] = {nullptr, nullptr};
   uint64_t stage_pairs = 0;
@@ -147,13 +156,16 @@ static void free_all(Ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* dev[] = {c->pool, c->touch_own, c->active, c->aat, c->sa_cnt, c->sa_list, c->sa_bits,
-                 c->counters, c->ws, c->cand, c->rep, c->rep_sorted, c->rep_above, c->keys,
+  void* dev[] = {c->pool, c->touch_own, c->active, c->scratch, c->sa_list, c->ws, c->cand, c->rep, c->rep_sorted, c->rep_above, c->keys,
                  c->keys_alt, c->vals, c->vals_alt, c->cub_tmp, c->export_buf, c->stage[0],
                  c->stage[1]};
   for (void* p : dev) if (p) cudaFree(p);
   if (c->h_counters) cudaFreeHost(c->h_counters);
+  if (c->h_clock) cudaFreeHost(c->h_clock);
+  if (c->d_clock) cudaFree(c->d_clock);
+  for (auto& row : c->graph) for (auto& g : row) if (g) cudaGraphExecDestroy(g);
   if (c->h_rep) cudaFreeHost(c->h_rep);
+  if (c->h_big) cudaFreeHost(c->h_big);
   for (int q = 0; q < 2; ++q) {
     if (c->ev_copied[q]) cudaEventDestroy(c->ev_copied[q]);
     if (c->ev_scanned[q]) cudaEventDestroy(c->ev_scanned[q]);
@@ -356,13 +368,44 @@ asse_status asse_init(const asse_config* cfg, void** out) {
   CKI(cudaMalloc(&c->pool, c->n_at * c->cb));
   CKI(cudaMalloc(&c->touch_own, bm_bytes));
   CKI(cudaMalloc(&c->active, bm_bytes));
-  CKI(cudaMalloc(&c->aat, (size_t)p.r * c->F * sizeof(unsigned long long)));
-  CKI(cudaMalloc(&c->sa_cnt, (size_t)p.r * c->F * 4));
+  {
+    const size_t aat_b = (size_t)p.r * c->F * 8, cnt_b = ((size_t)p.r * c->F * 4 + 255) & ~(size_t)255;
+    const size_t bits_b = (size_t)p.r * c->F * ((c->E + 31) / 32) * 4;
+    c->scratch_bytes = aat_b + cnt_b + 256 + bits_b;
+    CKI(cudaMalloc(&c->scratch, c->scratch_bytes));
+    uint8_t* b0 = (uint8_t*)c->scratch;
+    c->aat = (unsigned long long*)b0;
+    c->sa_cnt = (uint32_t*)(b0 + aat_b);
+    c->counters = (uint32_t*)(b0 + aat_b + cnt_b);
+    c->sa_bits = (uint32_t*)(b0 + aat_b + cnt_b + 256);
+  }
   CKI(cudaMalloc(&c->sa_list, (size_t)p.r * c->F * c->E * 4));
-  CKI(cudaMalloc(&c->sa_bits, (size_t)p.r * c->F * ((c->E + 31) / 32) * 4));
-  CKI(cudaMalloc(&c->counters, 64));
-  c->ws_cap = std::max<uint64_t>(p.max_candidates, 1u << 16);
-  CKI(cudaMalloc(&c->ws, (size_t)c->F * 2 * c->ws_cap * 4));
+  {
+    // restore geometry (Alg. 4 join plan), parts CTAs per frame
+    RestoreParams& rp = c->rp0;
+    rp.max_cand = p.max_candidates;
+    rp.r = p.r; rp.u = p.u; rp.c = p.c; rp.W = c->W; rp.F = c->F;
+    rp.parts = (uint32_t)std::max<int>(1, std::min<int>(16, (2 * c->sms) / (int)c->F));
+    std::vector<uint8_t> known(c->W, 0);
+    for (uint32_t y = 0; y < p.r; ++y) {
+      rp.shift[y] = c->shift[y];
+      uint32_t ov = 0, nf = 0;
+      for (uint32_t j = 0; j < p.c; ++j) {
+        uint32_t pos = (c->shift[y] + j) % c->W;
+        if (known[pos]) ov |= 1u << j;
+        else rp.freepos[y][nf++] = (uint8_t)j;
+      }
+      for (uint32_t j = 0; j < p.c; ++j) known[(c->shift[y] + j) % c->W] = 1;
+      rp.ov[y] = ov;
+      rp.nfree[y] = nf;
+      rp.use_enum_max[y] = (nf <= 20) ? 4u : 0u;
+    }
+    c->restore_smem = (size_t)p.r * ((c->E + 31) / 32) * 4;
+    if (c->restore_smem > 48 * 1024)
+      CKI(cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->restore_smem));
+    c->ws_cap = 1u << 16;   // partial LBS per CTA and join level
+    CKI(cudaMalloc(&c->ws, (size_t)c->F * rp.parts * 2 * c->ws_cap * 4));
+  }
   CKI(cudaMalloc(&c->cand, (size_t)p.max_candidates * 4));
   CKI(cudaMalloc(&c->rep, (size_t)p.max_candidates * sizeof(ReportDev)));
   CKI(cudaMalloc(&c->rep_sorted, (size_t)p.max_candidates * sizeof(ReportDev)));
@@ -381,7 +424,10 @@ asse_status asse_init(const asse_config* cfg, void** out) {
     CKI(cudaMalloc(&c->cub_tmp, c->cub_bytes));
   }
   CKI(cudaMallocHost(&c->h_counters, 64));
-  c->h_rep_cap = 0;
+  CKI(cudaMallocHost(&c->h_clock, 64));
+  CKI(cudaMalloc(&c->d_clock, 64));
+  c->h_rep_cap = 4096;   // reports fetched together with the counters (one sync)
+  CKI(cudaMallocHost(&c->h_rep, c->h_rep_cap * sizeof(ReportDev)));
   for (auto& e : c->ev) CKI(cudaEventCreate(&e));
   for (int q = 0; q < 2; ++q) {
     CKI(cudaEventCreateWithFlags(&c->ev_copied[q], cudaEventDisableTiming));
@@ -515,6 +561,7 @@ static asse_status copy_reports(Ctx* c, asse_report* h_out, uint32_t cap, uint32
   if (n > cap) return ASSE_E_CAPACITY;
   if (c->h_rep_cap < n) {
     if (c->h_rep) cudaFreeHost(c->h_rep);
+  if (c->h_big) cudaFreeHost(c->h_big);
     c->h_rep = nullptr;
     c->h_rep_cap = std::max<uint64_t>(n, 4096);
     CK(cudaMallocHost(&c->h_rep, c->h_rep_cap * sizeof(ReportDev)));
@@ -527,17 +574,18 @@ static asse_status copy_reports(Ctx* c, asse_report* h_out, uint32_t cap, uint32
   return ASSE_OK;
 }
 
-asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
-  if (!ctx) return ASSE_E_PARAM;
-  Ctx* c = static_cast<Ctx*>(ctx);
-  if (n_out) *n_out = 0;
-  if (mode > 1) { c->err = "mode must be 0 or 1"; return ASSE_E_PARAM; }
-  if (closed_all(c)) { c->err = "all n_slices closed"; return ASSE_E_STATE; }
-  if (c->cfg.world > 1 && !c->peers) { c->err = "world > 1 requires asse_attach_peers"; return ASSE_E_PEER; }
-  CK(cudaSetDevice(c->device));
+// Every device operation of end_slice up to the result copies, in stream order. Used
+// eagerly (world > 1 with a device barrier) or captured once into a CUDA graph per
+// (timing, mode) and replayed every slice; the per-slice ACT base comes from d_clock.
+static asse_status enqueue_end_slice(Ctx* c, uint32_t mode, bool timing, bool capturing) {
   const asse_config& p = c->cfg;
   cudaStream_t s = c->stream;
-  if (c->timing) CK(cudaEventRecord(c->ev[0], s));
+  // events recorded inside a captured graph must be external event-record nodes
+  auto rec = [&](int i) {
+    return capturing ? cudaEventRecordWithFlags(c->ev[i], s, cudaEventRecordExternal)
+                     : cudaEventRecord(c->ev[i], s);
+  };
+  if (timing) CK(rec(0));
   // a5: merge (world > 1)
   const uint32_t* src = c->touch;
   if (c->peers) {
@@ -549,12 +597,9 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
     }
     src = c->merged;
   }
-  if (c->timing) CK(cudaEventRecord(c->ev[1], s));
+  if (timing) CK(rec(1));
   // a6: fold + weights + super + preserve(t+1)
-  CK(cudaMemsetAsync(c->aat, 0, (size_t)p.r * c->F * sizeof(unsigned long long), s));
-  CK(cudaMemsetAsync(c->sa_cnt, 0, (size_t)p.r * c->F * 4, s));
-  CK(cudaMemsetAsync(c->sa_bits, 0, (size_t)p.r * c->F * ((c->E + 31) / 32) * 4, s));
-  CK(cudaMemsetAsync(c->counters, 0, 64, s));
+  CK(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, s));   // AAT, SA counts/bits, counters
   {
     FoldParams fp{};
     fp.pool = c->pool;
@@ -567,69 +612,98 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
     fp.sa_bits = c->sa_bits;
     fp.n_super = c->counters + 3;
     fp.n_chunks = c->n_at / 512;
-    fp.g = p.g; fp.k = p.k; fp.kp = c->kp; fp.C0 = c->C0; fp.a = c->a;
+    fp.C0 = c->d_clock;
+    fp.g = p.g; fp.k = p.k; fp.kp = c->kp; fp.a = c->a;
     fp.c = p.c; fp.w_theta = c->w_theta; fp.lpa_log2 = c->lpa_log2;
     const uint64_t tiles = (fp.n_chunks + kFoldChunksPerTile - 1) / kFoldChunksPerTile;
     const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)c->fold_grid));
-    if (c->timing) CK(cudaEventRecord(c->ev[2], s));
+    if (timing) CK(rec(2));
     if (c->cb == 1) launch_fold<1>(c->lpa_log2, (unsigned)blocks, s, fp);
     else launch_fold<2>(c->lpa_log2, (unsigned)blocks, s, fp);
     CK(cudaGetLastError());
-    LAUNCHED(c);
-    c->stats.fold_launches++;
-    if (c->timing) CK(cudaEventRecord(c->ev[3], s));
+    if (timing) CK(rec(3));
   }
-  // a7: restore (Alg. 4), one CTA per frame
+  // a7: restore (Alg. 4): parts CTAs per frame
   {
-    RestoreParams rp{};
+    RestoreParams rp = c->rp0;
     rp.sa_cnt = c->sa_cnt; rp.sa_list = c->sa_list; rp.sa_bits = c->sa_bits;
     rp.ws = c->ws; rp.ws_cap = c->ws_cap;
     rp.cand = c->cand; rp.n_cand = c->counters + 0; rp.overflow = c->counters + 1;
-    rp.max_cand = p.max_candidates;
-    rp.r = p.r; rp.u = p.u; rp.c = p.c; rp.W = c->W; rp.F = c->F;
-    std::vector<uint8_t> known(c->W, 0);
-    for (uint32_t y = 0; y < p.r; ++y) {
-      rp.shift[y] = c->shift[y];
-      uint32_t ov = 0, nf = 0;
-      for (uint32_t j = 0; j < p.c; ++j) {
-        uint32_t pos = (c->shift[y] + j) % c->W;
-        if (known[pos]) ov |= 1u << j;
-        else rp.freepos[y][nf++] = (uint8_t)j;
-      }
-      for (uint32_t j = 0; j < p.c; ++j) known[(c->shift[y] + j) % c->W] = 1;
-      rp.ov[y] = ov;
-      rp.nfree[y] = nf;
-      rp.use_enum_max[y] = (nf <= 20) ? 4u : 0u;
-    }
-    size_t smem = (size_t)p.r * ((c->E + 31) / 32) * 4;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (c->timing) CK(cudaEventRecord(c->ev[4], s));
-    k_restore<<<c->F, 512, smem, s>>>(rp);
+    if (timing) CK(rec(4));
+    k_restore<<<c->F * rp.parts, 512, c->restore_smem, s>>>(rp);
     CK(cudaGetLastError());
-    LAUNCHED(c);
-    if (c->timing) CK(cudaEventRecord(c->ev[5], s));
+    if (timing) CK(rec(5));
   }
-  CK(cudaMemcpyAsync(c->h_counters, c->counters, 16, cudaMemcpyDeviceToHost, s));
+  // a8: NAT + Eq. 5 over |CSIP| read on the device, then the sorts by ip
+  if (timing) CK(rec(6));
+  {
+    NatParams np{};
+    np.cand = c->cand; np.active = c->active; np.aat = c->aat; np.reports = c->rep;
+    np.keys = c->keys; np.vals = c->vals; np.n_above = c->counters + 2;
+    np.n_cand = c->counters + 0; np.max_cand = p.max_candidates;
+    np.A_inv = c->A_inv; np.r = p.r; np.u = p.u; np.c = p.c; np.W = c->W; np.F = c->F;
+    np.g = p.g; np.wpa = c->wpa; np.theta = p.theta; np.cells = (double)p.g * (double)c->E;
+    for (int y = 0; y < kMaxR; ++y) np.shift[y] = c->shift[y];
+    k_nat_est<<<(unsigned)c->sms * 2, 256, 0, s>>>(np);
+    CK(cudaGetLastError());
+  }
+  if (timing) CK(rec(7));
+  k_rank_sort<<<kRankBlocks, kRankThreads, 0, s>>>(c->rep, c->counters, p.max_candidates, c->rep_sorted, c->rep_above);
+  CK(cudaGetLastError());
+  k_sort_small<<<1, kSortThreads, 0, s>>>(c->rep, c->counters, p.max_candidates, c->rep_sorted, c->rep_above);
+  CK(cudaGetLastError());
+  if (timing) CK(rec(8));
+  return ASSE_OK;
+}
+static constexpr int kEndSliceKernels = 6;   // fold, restore, nat, rank sort, block sort (+ memset)
+
+asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (n_out) *n_out = 0;
+  if (mode > 1) { c->err = "mode must be 0 or 1"; return ASSE_E_PARAM; }
+  if (closed_all(c)) { c->err = "all n_slices closed"; return ASSE_E_STATE; }
+  if (c->cfg.world > 1 && !c->peers) { c->err = "world > 1 requires asse_attach_peers"; return ASSE_E_PEER; }
+  CK(cudaSetDevice(c->device));
+  const asse_config& p = c->cfg;
+  cudaStream_t s = c->stream;
+  const bool timing = c->timing;
+  const uint32_t K = (uint32_t)std::min<uint64_t>(c->h_rep_cap, p.max_candidates);
+  // the per-slice ACT base reaches the kernels through device memory, so the captured
+  // graph is identical for every slice (host copies stay outside the graph)
+  *c->h_clock = c->C0;
+  CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
+  if (c->peers && c->sync_mode == 0) {
+    asse_status st = enqueue_end_slice(c, mode, timing, false);   // the barrier epoch changes per slice
+    if (st != ASSE_OK) return st;
+  } else {
+    cudaGraphExec_t& ge = c->graph[timing ? 1 : 0][mode];
+    if (!ge) {
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      asse_status st = enqueue_end_slice(c, mode, timing, true);
+      cudaError_t ce = cudaStreamEndCapture(s, &g);
+      if (st != ASSE_OK) { if (g) cudaGraphDestroy(g); return st; }
+      CK(ce);
+      CK(cudaGraphInstantiate(&ge, g, 0));
+      CK(cudaGraphDestroy(g));
+    }
+    CK(cudaGraphLaunch(ge, s));
+  }
+  // results: counters plus a prefix of the requested report array, one synchronisation
+  CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(c->h_rep, mode ? c->rep_sorted : c->rep_above, (size_t)K * sizeof(ReportDev),
+                     cudaMemcpyDeviceToHost, s));
+  if (timing) CK(cudaEventRecord(c->ev[9], s));
+  c->stats.kernel_launches += kEndSliceKernels - 1 + (c->peers && c->sync_mode == 0 ? 3 : 0);
+  c->stats.fold_launches++;
   CK(cudaStreamSynchronize(s));
   const uint32_t n_cand_raw = c->h_counters[0];
   const bool overflow = c->h_counters[1] != 0 || n_cand_raw > p.max_candidates;
   const uint32_t n_cand = overflow ? 0 : n_cand_raw;
-  // a8: NAT + Eq. 5, sort by ip, compaction of est >= theta
-  if (c->timing) CK(cudaEventRecord(c->ev[6], s));
-  if (n_cand > 0) {
-    NatParams np{};
-    np.cand = c->cand; np.active = c->active; np.aat = c->aat; np.reports = c->rep;
-    np.keys = c->keys; np.vals = c->vals; np.n_above = c->counters + 2; np.n = n_cand;
-    np.A_inv = c->A_inv; np.r = p.r; np.u = p.u; np.c = p.c; np.W = c->W; np.F = c->F;
-    np.g = p.g; np.wpa = c->wpa; np.theta = p.theta; np.cells = (double)p.g * (double)c->E;
-    for (int y = 0; y < kMaxR; ++y) np.shift[y] = c->shift[y];
-    unsigned blocks = (unsigned)std::min<uint64_t>((n_cand + 255) / 256, (uint64_t)c->sms * 8);
-    k_nat_est<<<blocks, 256, 0, s>>>(np);
-    CK(cudaGetLastError());
-    LAUNCHED(c);
-  }
-  if (c->timing) CK(cudaEventRecord(c->ev[7], s));
-  if (n_cand > 0) {
+  bool prefetched = true;
+  if (!overflow && c->h_counters[5]) {
+    // |CSIP| above the block-sort capacity: device-wide radix sort (needs n on the host)
     cub::DoubleBuffer<uint32_t> dk(c->keys, c->keys_alt), dv(c->vals, c->vals_alt);
     size_t bytes = c->cub_bytes;
     CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, dk, dv, (int)n_cand, 0, 32, s));
@@ -642,11 +716,10 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
     CK(cub::DeviceSelect::If(c->cub_tmp, bytes, c->rep_sorted, c->rep_above, c->counters + 4,
                              (int)n_cand, AboveTheta(), s));
     c->stats.kernel_launches += 2;
+    CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    prefetched = false;
   }
-  if (c->timing) CK(cudaEventRecord(c->ev[8], s));
-  CK(cudaMemcpyAsync(c->h_counters, c->counters, 32, cudaMemcpyDeviceToHost, s));
-  if (c->timing) CK(cudaEventRecord(c->ev[9], s));
-  CK(cudaStreamSynchronize(s));
   c->last_n = n_cand;
   c->last_above = n_cand ? c->h_counters[4] : 0;
   c->have_reports = true;
@@ -673,6 +746,14 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
     c->last_n = c->last_above = 0;
     c->err = "CSIP exceeded max_candidates (or the restore join workspace)";
     return ASSE_E_OVERFLOW;
+  }
+  const uint32_t n = mode ? c->last_n : c->last_above;
+  if (prefetched && n <= K) {
+    if (n_out) *n_out = n;
+    if (!h_out) return n > cap ? ASSE_E_CAPACITY : ASSE_OK;
+    if (n > cap) return ASSE_E_CAPACITY;
+    memcpy(h_out, c->h_rep, (size_t)n * sizeof(ReportDev));
+    return ASSE_OK;
   }
   return copy_reports(c, h_out, cap, n_out, mode);
 }

@@ -13,6 +13,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "asse_tma.cuh"
 
 namespace asse {
@@ -184,7 +186,8 @@ struct FoldParams {
   uint32_t* sa_bits;          // out: SA(y,z) membership bits, pre-zeroed
   uint32_t* n_super;          // out: total super ATVs
   uint64_t n_chunks;          // pool ATs / 512
-  uint32_t g, k, kp, C0, a;   // ATV size, window, k', ACT base, block size a (A7)
+  const uint32_t* C0;         // ACT base of block 0 for this slice (device scalar)
+  uint32_t g, k, kp, a;       // ATV size, window, k', block size a (A7)
   uint32_t c, w_theta;        // column bits, integer super threshold (A15)
   uint32_t lpa_log2;          // log2(lanes per ATV) = log2(g/16)
 };
@@ -278,6 +281,7 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
   }
   const uint32_t lia = lane & (LPA - 1u);           // lane within its ATV
   const uint32_t two_k = 2u * p.k;
+  const uint32_t C0 = *p.C0;
 
   // ---- per-lane, per-element constants (positions i = 16*lia + e), computed once
   uint32_t CLK[NW], LO1[NW], HI1[NW], LO2[NW], HI2[NW], LE1[NW], HE1[NW], LE2[NW], HE2[NW];
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
     for (int e = 0; e < EPW; ++e) {
       const uint32_t i = 16u * lia + (uint32_t)(q * EPW + e);
       uint32_t blk = (p.a > 0) ? min(i / p.a, two_k - 1u) : two_k - 1u;  // A7
-      uint32_t clk = (p.C0 + blk) % two_k;
+      uint32_t clk = (C0 + blk) % two_k;
       uint32_t lo1, hi1 = clk, lo2, hi2;
       if (clk + 1u >= p.kp) { lo1 = clk + 1u - p.kp; lo2 = S::EMPTY_LO; hi2 = 0; }
       else { lo1 = 0; lo2 = clk + 1u + two_k - p.kp; hi2 = two_k - 1u; }
@@ -421,8 +425,9 @@ struct RestoreParams {
   const uint32_t* sa_cnt;   // [r*F]
   const uint32_t* sa_list;  // [r*F][E]
   const uint32_t* sa_bits;  // [r*F][E/32]
-  uint32_t* ws;             // join workspace: F frames x 2 buffers x ws_cap
+  uint32_t* ws;             // join workspace: (F * parts) CTAs x 2 buffers x ws_cap
   uint64_t ws_cap;
+  uint32_t parts;           // CTAs per frame: row 0's candidates are split among them
   uint32_t* cand;           // out: candidates as mangled values h = (LBS << u) | z
   uint32_t* n_cand;         // out: |CSIP|
   uint32_t* overflow;       // out: 1 if CSIP or a join level exceeded its capacity
@@ -442,7 +447,7 @@ __device__ __forceinline__ uint32_t place_row(uint32_t x, uint32_t sh, uint32_t 
   return (uint32_t)((P | (P >> W)) & wmask);
 }
 
-// Alg. 4 per frame z (one CTA): CSIP_z = {LBS : x_y(LBS) in SA(y, z) for all y}.
+// Alg. 4 per frame z (parts CTAs, each taking every parts-th row-0 candidate): CSIP_z = {LBS : x_y(LBS) in SA(y, z) for all y}.
 // The r-fold product of P:364 is evaluated as a join: rows are added one at a time,
 // and a partial LBS only survives when every duplicate position agrees,
 // which yields exactly the tuples that pass Alg. 4's check (A16). Row y either scans
@@ -452,7 +457,8 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
   extern __shared__ uint32_t s_bits[];  // r * E/32 words of SA(y, z) membership
   __shared__ uint32_t s_next;
   __shared__ uint32_t s_nin;
-  const uint32_t z = blockIdx.x;
+  const uint32_t z = blockIdx.x / p.parts;
+  const uint32_t part = blockIdx.x % p.parts;
   const uint32_t E = 1u << p.c;
   const uint32_t ew = (E + 31u) >> 5;
   const uint32_t cmask = (p.c >= 32) ? 0xFFFFFFFFu : ((1u << p.c) - 1u);
@@ -460,7 +466,8 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
     uint32_t y = q / ew, w = q % ew;
     s_bits[q] = p.sa_bits[((size_t)y * p.F + z) * ew + w];
   }
-  uint32_t* buf[2] = {p.ws + (size_t)z * 2 * p.ws_cap, p.ws + (size_t)z * 2 * p.ws_cap + p.ws_cap};
+  uint32_t* buf[2] = {p.ws + (size_t)blockIdx.x * 2 * p.ws_cap,
+                      p.ws + (size_t)blockIdx.x * 2 * p.ws_cap + p.ws_cap};
   if (threadIdx.x == 0) { s_nin = 1; buf[0][0] = 0; }
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31u;
@@ -477,7 +484,9 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
     const bool last = (y + 1 == p.r);
     const uint32_t nf = p.nfree[y];
     const bool use_enum = ((1ull << nf) <= (uint64_t)p.use_enum_max[y] * nsa);
-    const uint64_t per = use_enum ? (1ull << nf) : (uint64_t)nsa;
+    const uint64_t n_opt = use_enum ? (1ull << nf) : (uint64_t)nsa;
+    // row 0 (single empty partial): this CTA takes options part, part + parts, ...
+    const uint64_t per = (y == 0) ? (n_opt > part ? (n_opt - part + p.parts - 1) / p.parts : 0) : n_opt;
     const uint64_t total = (uint64_t)n_in * per;
     const uint32_t* in = buf[y & 1];
     uint32_t* out = buf[(y + 1) & 1];
@@ -489,7 +498,7 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
       uint32_t nl = 0;
       if (idx < total) {
         const uint32_t L = in[idx / per];
-        const uint32_t sub = (uint32_t)(idx % per);
+        const uint32_t sub = (y == 0) ? (uint32_t)(part + (idx % per) * p.parts) : (uint32_t)(idx % per);
         const uint64_t D = (uint64_t)L | ((uint64_t)L << p.W);
         const uint32_t xk = (uint32_t)(D >> p.shift[y]) & cmask;
         uint32_t x;
@@ -544,7 +553,8 @@ struct NatParams {
   uint32_t* keys;              // ip, for the sort
   uint32_t* vals;              // index, for the sort
   uint32_t* n_above;
-  uint32_t n;
+  const uint32_t* n_cand;      // |CSIP| (device), clamped to max_cand
+  uint32_t max_cand;
   uint32_t A_inv, r, u, c, W, F, g, wpa;
   double theta, cells;         // cells = g * 2^c
   uint32_t shift[kMaxR];
@@ -555,49 +565,55 @@ struct ReportDev { uint32_t ip, nat; double estimate; uint32_t flags, pad; };
 // Alg. 5 NAT as an AND of the r active bit rows + popcount, UP (Eq. 4,
 // P:412) from AAT in double, Eq. 5 (A19), flags (A20, A21).
 __global__ void __launch_bounds__(256) k_nat_est(NatParams p) {
+  // LPC lanes per candidate: lane j of a group reads the j-th 16-byte word of each of
+  // the r active rows (independent loads), ANDs them and the group sums popcounts.
+  const uint32_t lpc = p.wpa / 4;                   // 1, 2 or 4 (g = 128, 256, 512)
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t sub = lane & (lpc - 1u);
   const uint32_t fmask = (1u << p.u) - 1u;
   const uint32_t cmask = (1u << p.c) - 1u;
-  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < p.n; q += gridDim.x * blockDim.x) {
-    const uint32_t h = p.cand[q];
-    const uint32_t z = h & fmask;
-    const uint64_t L = (uint64_t)(h >> p.u);
-    const uint64_t D = L | (L << p.W);
-    const uint4* rows[kMaxR];
+  const uint32_t n = min(*p.n_cand, p.max_cand);
+  const uint32_t groups_per_grid = (gridDim.x * blockDim.x) / lpc;
+  const uint32_t g0 = (blockIdx.x * blockDim.x + threadIdx.x) / lpc;
+  const uint32_t rounds = (n + groups_per_grid - 1) / groups_per_grid;
+  for (uint32_t rd = 0; rd < rounds; ++rd) {
+    const uint32_t q = g0 + rd * groups_per_grid;
+    const bool valid = q < n;
+    uint32_t nat = 0, h = 0, z = 0;
+    if (valid) {
+      h = p.cand[q];
+      z = h & fmask;
+      const uint64_t L = (uint64_t)(h >> p.u);
+      const uint64_t D = L | (L << p.W);
+      uint4 a = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
 #pragma unroll
-    for (int y = 0; y < kMaxR; ++y) {
-      if (y < (int)p.r) {
-        uint32_t x = (uint32_t)(D >> p.shift[y]) & cmask;
-        size_t atv = (((size_t)y * p.F + z) << p.c) | x;
-        rows[y] = reinterpret_cast<const uint4*>(p.active + atv * p.wpa);
-      }
-    }
-    uint32_t nat = 0;
-    for (uint32_t w4 = 0; w4 < p.wpa / 4; ++w4) {
-      uint4 a = __ldcg(rows[0] + w4);
-#pragma unroll
-      for (int y = 1; y < kMaxR; ++y) {
+      for (int y = 0; y < kMaxR; ++y) {
         if (y < (int)p.r) {
-          uint4 b = __ldcg(rows[y] + w4);
+          const uint32_t x = (uint32_t)(D >> p.shift[y]) & cmask;
+          const size_t atv = (((size_t)y * p.F + z) << p.c) | x;
+          const uint4 b = __ldcg(reinterpret_cast<const uint4*>(p.active + atv * p.wpa) + sub);
           a.x &= b.x; a.y &= b.y; a.z &= b.z; a.w &= b.w;
         }
       }
-      nat += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+      nat = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
     }
-    double up = 0.0;
-    for (uint32_t y = 0; y < p.r; ++y) {
-      double P = (double)p.aat[y * p.F + z] / p.cells;   // P_{y,z}^{k'}
-      up = (y == 0) ? P : up * P;                          // UP = prod_y P
+    for (uint32_t off = 1; off < lpc; off <<= 1) nat += __shfl_xor_sync(0xFFFFFFFFu, nat, off);
+    if (valid && sub == 0) {
+      double up = 0.0;
+      for (uint32_t y = 0; y < p.r; ++y) {
+        const double P = (double)p.aat[y * p.F + z] / p.cells;   // P_{y,z}^{k'}
+        up = (y == 0) ? P : up * P;                                // UP = prod_y P
+      }
+      double est;
+      if (nat == p.g) est = __longlong_as_double(0x7FF0000000000000LL);   // +inf (A20)
+      else est = -(double)p.g * log((double)(p.g - nat) / ((double)p.g * (1.0 - up)));
+      const uint32_t flags = (nat == p.g ? 1u : 0u) | (est >= p.theta ? 2u : 0u);
+      const uint32_t ip = p.A_inv * h;                               // f^{-1}
+      ReportDev* R = reinterpret_cast<ReportDev*>(p.reports) + q;
+      R->ip = ip; R->nat = nat; R->estimate = est; R->flags = flags; R->pad = 0;
+      p.keys[q] = ip;
+      p.vals[q] = q;
     }
-    double est;
-    if (nat == p.g) est = __longlong_as_double(0x7FF0000000000000LL);  // +inf (A20)
-    else est = -(double)p.g * log((double)(p.g - nat) / ((double)p.g * (1.0 - up)));
-    uint32_t flags = (nat == p.g ? 1u : 0u) | (est >= p.theta ? 2u : 0u);
-    const uint32_t ip = p.A_inv * h;                       // f^{-1}
-    ReportDev* R = reinterpret_cast<ReportDev*>(p.reports) + q;
-    R->ip = ip; R->nat = nat; R->estimate = est; R->flags = flags; R->pad = 0;
-    p.keys[q] = ip;
-    p.vals[q] = q;
-    if (flags & 2u) atomicAdd(p.n_above, 1u);
   }
 }
 
@@ -606,6 +622,134 @@ __global__ void k_gather(const ReportDev* __restrict__ in, const uint32_t* __res
                          uint32_t n, ReportDev* __restrict__ out_all) {
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
     out_all[q] = in[order[q]];
+}
+
+// Sort of a small CSIP by ip (A24) inside one CTA (block radix sort in shared
+// memory), then the ascending-ip report array and its est >= theta subset (A21).
+// If |CSIP| exceeds the block capacity it only raises *big (the host then runs the
+// device-wide radix sort). counters: [0] n_cand, [2] n_above, [4] n_sel, [5] big.
+constexpr int kSortThreads = 512;
+constexpr uint32_t kSortCap = kSortThreads * 16;   // 8192
+
+template <int ITEMS>
+__device__ __forceinline__ void sort_and_emit(const ReportDev* __restrict__ rep, uint32_t n,
+                                              ReportDev* __restrict__ sorted, ReportDev* __restrict__ above,
+                                              uint32_t* counters, void* tmp_raw, uint32_t* warp_cnt) {
+  using BlockSort = cub::BlockRadixSort<uint32_t, kSortThreads, ITEMS, uint32_t, 4>;
+  auto& tmp = *reinterpret_cast<typename BlockSort::TempStorage*>(tmp_raw);
+  uint32_t keys[ITEMS], idx[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t q = threadIdx.x * ITEMS + j;       // blocked arrangement
+    keys[j] = (q < n) ? rep[q].ip : 0xFFFFFFFFu;
+    idx[j] = q;
+  }
+  BlockSort(tmp).Sort(keys, idx);                        // stable, ascending
+  uint32_t mine = 0;
+  uint32_t sel[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t q = threadIdx.x * ITEMS + j;
+    sel[j] = 0;
+    if (q < n) {
+      const ReportDev r = rep[idx[j]];
+      sorted[q] = r;
+      sel[j] = (r.flags & 2u) ? 1u : 0u;
+      mine += sel[j];
+    }
+  }
+  // exclusive prefix over threads (thread order == ip order in the blocked layout)
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  uint32_t incl = mine;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+    if (lane >= (uint32_t)off) incl += t;
+  }
+  if (lane == 31) warp_cnt[wid] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int w = 0; w < kSortThreads / 32; ++w) { const uint32_t t = warp_cnt[w]; warp_cnt[w] = acc; acc += t; }
+    counters[4] = acc;
+    counters[5] = 0u;
+  }
+  __syncthreads();
+  uint32_t pos = warp_cnt[wid] + incl - mine;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t q = threadIdx.x * ITEMS + j;
+    if (q < n && sel[j]) above[pos++] = rep[idx[j]];
+  }
+}
+
+// Rank sort for |CSIP| <= 2048 (one CTA): CSIP ips are distinct (a tuple <-> LBS
+// bijection, A16), so an element's position is the number of smaller ips; its position
+// among the est >= theta reports counts the smaller ips flagged ABOVE_THETA.
+constexpr int kRankThreads = 256;
+constexpr uint32_t kRankCap = 2048;
+constexpr int kRankBlocks = kRankCap / (kRankThreads / 32);   // one warp per element
+__global__ void __launch_bounds__(kRankThreads) k_rank_sort(const ReportDev* __restrict__ rep,
+                                                            uint32_t* counters, uint32_t max_cand,
+                                                            ReportDev* __restrict__ sorted,
+                                                            ReportDev* __restrict__ above) {
+  __shared__ uint32_t s_key[kRankCap];
+  __shared__ uint32_t s_above[kRankCap / 32];   // ABOVE_THETA flags as a bitset
+  const uint32_t n = min(counters[0], max_cand);
+  if (n > kRankCap || n == 0) return;
+  const uint32_t q = blockIdx.x * (kRankThreads / 32) + (threadIdx.x >> 5);
+  if (blockIdx.x * (kRankThreads / 32) >= n) return;       // CTA without elements
+  for (uint32_t j = threadIdx.x; j < kRankCap / 32; j += kRankThreads) s_above[j] = 0;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < n; j += kRankThreads) {
+    const ReportDev r = rep[j];
+    s_key[j] = r.ip;
+    if (r.flags & 2u) atomicOr(&s_above[j >> 5], 1u << (j & 31u));
+  }
+  __syncthreads();
+  if (q >= n) return;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t k = s_key[q];
+  uint32_t r_all = 0, r_above = 0;
+  for (uint32_t j = lane; j < n; j += 32) {
+    const uint32_t less = s_key[j] < k ? 1u : 0u;
+    r_all += less;
+    r_above += less & (s_above[j >> 5] >> (j & 31u));
+  }
+  r_all = __reduce_add_sync(0xFFFFFFFFu, r_all);
+  r_above = __reduce_add_sync(0xFFFFFFFFu, r_above);
+  if (lane == 0) {
+    const ReportDev r = rep[q];
+    sorted[r_all] = r;
+    if (r.flags & 2u) {
+      above[r_above] = r;
+      atomicAdd(counters + 4, 1u);
+    }
+  }
+}
+
+// Sort of a small CSIP by ip (A24) inside one CTA (block radix sort, 4-bit digits, item
+// count picked from |CSIP| read on the device), then the ascending-ip report array and
+// its est >= theta subset (A21). If |CSIP| exceeds the block capacity it only raises
+// counters[5] and the host runs the device-wide radix sort.
+// counters: [0] n_cand, [4] n_above, [5] big.
+__global__ void __launch_bounds__(kSortThreads) k_sort_small(const ReportDev* __restrict__ rep,
+                                                             uint32_t* counters, uint32_t max_cand,
+                                                             ReportDev* __restrict__ sorted,
+                                                             ReportDev* __restrict__ above) {
+  using S16 = cub::BlockRadixSort<uint32_t, kSortThreads, 16, uint32_t, 4>;
+  __shared__ __align__(16) typename S16::TempStorage tmp;   // the largest instance
+  __shared__ uint32_t warp_cnt[kSortThreads / 32];
+  const uint32_t n = min(counters[0], max_cand);
+  if (n <= kRankCap) return;                                 // k_rank_sort's case
+  if (n > kSortCap) {
+    if (threadIdx.x == 0) counters[5] = 1u;
+    return;
+  }
+  if (n <= kSortThreads * 2) sort_and_emit<2>(rep, n, sorted, above, counters, &tmp, warp_cnt);
+  else if (n <= kSortThreads * 4) sort_and_emit<4>(rep, n, sorted, above, counters, &tmp, warp_cnt);
+  else if (n <= kSortThreads * 8) sort_and_emit<8>(rep, n, sorted, above, counters, &tmp, warp_cnt);
+  else sort_and_emit<16>(rep, n, sorted, above, counters, &tmp, warp_cnt);
 }
 
 // --------------------------------------------------------------- export
