@@ -68,7 +68,9 @@ typedef struct {
   double scan_ms_total;          /* cumulative k_scan device time (timing enabled only) */
   double fold_ms_total;          /* cumulative k_fold device time (timing enabled only) */
   uint64_t fold_launches;
-  double last_merge_ms, last_fold_ms, last_restore_ms, last_nat_ms, last_sort_ms;
+  double last_merge_ms, last_fold_ms;
+  double last_restore_ms;        /* restore + NAT/Eq. 5 + sort (launched back to back) */
+  double last_nat_ms, last_sort_ms;  /* 0: fused into last_restore_ms */
   double last_end_slice_ms;      /* device time of the whole last end_slice */
   uint32_t last_n_super;         /* super ATVs in the last slice, all rows/frames */
   uint32_t last_n_candidates;    /* |CSIP| of the last slice */

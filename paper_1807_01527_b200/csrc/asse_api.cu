@@ -196,6 +196,24 @@ static void launch_fold(uint32_t lpal, unsigned blocks, cudaStream_t s, const Fo
   else k_fold<CB, 5><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may start while the
+// previous kernel in the stream drains; it waits with griddepcontrol.wait.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cudaStream_t st) {
   if (n == 0) return ASSE_OK;
   ScanParams p{};
@@ -385,6 +403,8 @@ asse_status asse_init(const asse_config* cfg, void** out) {
     RestoreParams& rp = c->rp0;
     rp.max_cand = p.max_candidates;
     rp.r = p.r; rp.u = p.u; rp.c = p.c; rp.W = c->W; rp.F = c->F;
+    rp.A_inv = c->A_inv; rp.g = p.g; rp.wpa = c->wpa; rp.theta = p.theta;
+    rp.cells = (double)p.g * (double)c->E;
     rp.parts = (uint32_t)std::max<int>(1, std::min<int>(16, (2 * c->sms) / (int)c->F));
     std::vector<uint8_t> known(c->W, 0);
     for (uint32_t y = 0; y < p.r; ++y) {
@@ -623,39 +643,23 @@ static asse_status enqueue_end_slice(Ctx* c, uint32_t mode, bool timing, bool ca
     CK(cudaGetLastError());
     if (timing) CK(rec(3));
   }
-  // a7: restore (Alg. 4): parts CTAs per frame
+  // a7 + a8: restore (Alg. 4, parts CTAs per frame) with NAT and Eq. 5 fused, then the
+  // sort by ip; both are launched with programmatic dependent launch so their launch
+  // overlaps the previous kernel's tail (griddepcontrol.wait inside).
   {
     RestoreParams rp = c->rp0;
     rp.sa_cnt = c->sa_cnt; rp.sa_list = c->sa_list; rp.sa_bits = c->sa_bits;
     rp.ws = c->ws; rp.ws_cap = c->ws_cap;
     rp.cand = c->cand; rp.n_cand = c->counters + 0; rp.overflow = c->counters + 1;
-    if (timing) CK(rec(4));
-    k_restore<<<c->F * rp.parts, 512, c->restore_smem, s>>>(rp);
-    CK(cudaGetLastError());
-    if (timing) CK(rec(5));
+    rp.active = c->active; rp.aat = c->aat; rp.reports = c->rep; rp.keys = c->keys; rp.vals = c->vals;
+    CK(launch_pdl(k_restore, dim3(c->F * rp.parts), dim3(512), c->restore_smem, s, rp));
   }
-  // a8: NAT + Eq. 5 over |CSIP| read on the device, then the sorts by ip
-  if (timing) CK(rec(6));
-  {
-    NatParams np{};
-    np.cand = c->cand; np.active = c->active; np.aat = c->aat; np.reports = c->rep;
-    np.keys = c->keys; np.vals = c->vals; np.n_above = c->counters + 2;
-    np.n_cand = c->counters + 0; np.max_cand = p.max_candidates;
-    np.A_inv = c->A_inv; np.r = p.r; np.u = p.u; np.c = p.c; np.W = c->W; np.F = c->F;
-    np.g = p.g; np.wpa = c->wpa; np.theta = p.theta; np.cells = (double)p.g * (double)c->E;
-    for (int y = 0; y < kMaxR; ++y) np.shift[y] = c->shift[y];
-    k_nat_est<<<(unsigned)c->sms * 2, 256, 0, s>>>(np);
-    CK(cudaGetLastError());
-  }
-  if (timing) CK(rec(7));
-  k_rank_sort<<<kRankBlocks, kRankThreads, 0, s>>>(c->rep, c->counters, p.max_candidates, c->rep_sorted, c->rep_above);
-  CK(cudaGetLastError());
-  k_sort_small<<<1, kSortThreads, 0, s>>>(c->rep, c->counters, p.max_candidates, c->rep_sorted, c->rep_above);
-  CK(cudaGetLastError());
+  CK(launch_pdl(k_sort, dim3(kSortBlocks), dim3(kSortThreads), 0, s, (const ReportDev*)c->rep, c->counters,
+                (uint32_t)p.max_candidates, c->rep_sorted, c->rep_above));
   if (timing) CK(rec(8));
   return ASSE_OK;
 }
-static constexpr int kEndSliceKernels = 6;   // fold, restore, nat, rank sort, block sort (+ memset)
+static constexpr int kEndSliceKernels = 3;   // fold, restore (+NAT), sort
 
 asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
   if (!ctx) return ASSE_E_PARAM;
@@ -695,7 +699,7 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
   CK(cudaMemcpyAsync(c->h_rep, mode ? c->rep_sorted : c->rep_above, (size_t)K * sizeof(ReportDev),
                      cudaMemcpyDeviceToHost, s));
   if (timing) CK(cudaEventRecord(c->ev[9], s));
-  c->stats.kernel_launches += kEndSliceKernels - 1 + (c->peers && c->sync_mode == 0 ? 3 : 0);
+  c->stats.kernel_launches += kEndSliceKernels + (c->peers && c->sync_mode == 0 ? 3 : 0);
   c->stats.fold_launches++;
   CK(cudaStreamSynchronize(s));
   const uint32_t n_cand_raw = c->h_counters[0];
@@ -731,9 +735,10 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
     CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1])); c->stats.last_merge_ms = ms;
     CK(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3])); c->stats.last_fold_ms = ms;
     c->stats.fold_ms_total += ms;
-    CK(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5])); c->stats.last_restore_ms = ms;
-    CK(cudaEventElapsedTime(&ms, c->ev[6], c->ev[7])); c->stats.last_nat_ms = ms;
-    CK(cudaEventElapsedTime(&ms, c->ev[7], c->ev[8])); c->stats.last_sort_ms = ms;
+    // restore + NAT + sort run back to back under programmatic dependent launch
+    CK(cudaEventElapsedTime(&ms, c->ev[3], c->ev[8])); c->stats.last_restore_ms = ms;
+    c->stats.last_nat_ms = 0;
+    c->stats.last_sort_ms = 0;
     CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[9])); c->stats.last_end_slice_ms = ms;
     asse_status hs = harvest_scan_timing(c);
     if (hs != ASSE_OK) return hs;

@@ -438,7 +438,19 @@ struct RestoreParams {
   uint32_t nfree[kMaxR];    // c - popc(ov[y])
   uint32_t use_enum_max[kMaxR];  // enumerate the 2^nfree completions when 2^nfree <= this * |SA|
   uint8_t freepos[kMaxR][32];    // free bit positions of x_y
+  // Alg. 5 / Eq. 5 for every restored candidate (fused)
+  const uint32_t* active;        // active bits, wpa words per ATV
+  const unsigned long long* aat; // AAT[y][z]
+  void* reports;                 // asse_report per CSIP slot
+  uint32_t* keys;                // ip per slot (device-wide sort)
+  uint32_t* vals;                // slot index (device-wide sort)
+  uint32_t A_inv, g, wpa;
+  double theta, cells;           // cells = g * 2^c
 };
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+struct ReportDev { uint32_t ip, nat; double estimate; uint32_t flags, pad; };
 
 __device__ __forceinline__ uint32_t place_row(uint32_t x, uint32_t sh, uint32_t W) {
   // LBS bits (sh + j) mod W <- x[j] (P:324 wrap-around)
@@ -453,34 +465,47 @@ __device__ __forceinline__ uint32_t place_row(uint32_t x, uint32_t sh, uint32_t 
 // which yields exactly the tuples that pass Alg. 4's check (A16). Row y either scans
 // SA(y,z) comparing the already-fixed bits, or enumerates the 2^nfree completions of
 // x_y and tests SA membership — whichever is fewer probes.
+constexpr uint32_t kPartSmem = 2048;   // partial LBS kept in shared memory per level buffer
+
 __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
   extern __shared__ uint32_t s_bits[];  // r * E/32 words of SA(y, z) membership
-  __shared__ uint32_t s_next;
-  __shared__ uint32_t s_nin;
+  __shared__ uint32_t s_part[2][kPartSmem];
+  __shared__ uint32_t s_nsa[kMaxR];
+  __shared__ uint32_t s_next, s_nin;
+  __shared__ double s_up;
   const uint32_t z = blockIdx.x / p.parts;
   const uint32_t part = blockIdx.x % p.parts;
   const uint32_t E = 1u << p.c;
   const uint32_t ew = (E + 31u) >> 5;
   const uint32_t cmask = (p.c >= 32) ? 0xFFFFFFFFu : ((1u << p.c) - 1u);
+  // partial buffers: slots < kPartSmem in shared memory, the rest in the global workspace
+  uint32_t* gbuf[2] = {p.ws + (size_t)blockIdx.x * 2 * p.ws_cap,
+                       p.ws + (size_t)blockIdx.x * 2 * p.ws_cap + p.ws_cap};
+  pdl_wait();                                         // k_fold's SA lists, bits, AAT, active bits
+  if (threadIdx.x < p.r) s_nsa[threadIdx.x] = p.sa_cnt[threadIdx.x * p.F + z];
+  if (threadIdx.x == 0) {
+    // UP_{k'}^{z} = prod_y AAT[y][z] / (g 2^c) (Eq. 4), same product order as the oracle
+    double up = 0.0;
+    for (uint32_t y = 0; y < p.r; ++y) {
+      const double P = (double)p.aat[y * p.F + z] / p.cells;
+      up = (y == 0) ? P : up * P;
+    }
+    s_up = up;
+    s_nin = 1;
+    s_part[0][0] = 0;
+  }
   for (uint32_t q = threadIdx.x; q < p.r * ew; q += blockDim.x) {
-    uint32_t y = q / ew, w = q % ew;
+    const uint32_t y = q / ew, w = q % ew;
     s_bits[q] = p.sa_bits[((size_t)y * p.F + z) * ew + w];
   }
-  uint32_t* buf[2] = {p.ws + (size_t)blockIdx.x * 2 * p.ws_cap,
-                      p.ws + (size_t)blockIdx.x * 2 * p.ws_cap + p.ws_cap};
-  if (threadIdx.x == 0) { s_nin = 1; buf[0][0] = 0; }
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31u;
   for (uint32_t y = 0; y < p.r; ++y) {
     const uint32_t n_in = s_nin;
-    const uint32_t nsa = p.sa_cnt[y * p.F + z];
+    const uint32_t nsa = s_nsa[y];
+    if (n_in == 0 || nsa == 0) break;                 // uniform across the CTA
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
-    if (n_in == 0 || nsa == 0) {
-      if (threadIdx.x == 0) s_nin = 0;
-      __syncthreads();
-      break;
-    }
     const bool last = (y + 1 == p.r);
     const uint32_t nf = p.nfree[y];
     const bool use_enum = ((1ull << nf) <= (uint64_t)p.use_enum_max[y] * nsa);
@@ -488,8 +513,7 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
     // row 0 (single empty partial): this CTA takes options part, part + parts, ...
     const uint64_t per = (y == 0) ? (n_opt > part ? (n_opt - part + p.parts - 1) / p.parts : 0) : n_opt;
     const uint64_t total = (uint64_t)n_in * per;
-    const uint32_t* in = buf[y & 1];
-    uint32_t* out = buf[(y + 1) & 1];
+    const uint32_t ib = y & 1u, ob = (y + 1) & 1u;
     const uint32_t* sal = p.sa_list + ((size_t)y * p.F + z) * E;
     const uint32_t* bits = s_bits + y * ew;
     const uint64_t rounded = (total + 31u) & ~31ull;
@@ -497,7 +521,8 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
       bool ok = false;
       uint32_t nl = 0;
       if (idx < total) {
-        const uint32_t L = in[idx / per];
+        const uint32_t pi = (uint32_t)(idx / per);
+        const uint32_t L = (pi < kPartSmem) ? s_part[ib][pi] : gbuf[ib][pi - kPartSmem];
         const uint32_t sub = (y == 0) ? (uint32_t)(part + (idx % per) * p.parts) : (uint32_t)(idx % per);
         const uint64_t D = (uint64_t)L | ((uint64_t)L << p.W);
         const uint32_t xk = (uint32_t)(D >> p.shift[y]) & cmask;
@@ -507,114 +532,69 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
           for (uint32_t b = 0; b < nf; ++b) x |= ((sub >> b) & 1u) << p.freepos[y][b];
           ok = (bits[x >> 5] >> (x & 31u)) & 1u;
         } else {
-          x = sal[sub];
+          x = __ldcg(sal + sub);
           ok = ((x ^ xk) & p.ov[y]) == 0;
         }
         nl = L | place_row(x, p.shift[y], p.W);
       }
       // warp-aggregated append
       const uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
-      if (m) {
-        const uint32_t rank = __popc(m & ((1u << lane) - 1u));
-        uint32_t base = 0;
-        const uint32_t leader = __ffs(m) - 1;
-        if (last) {
-          if (lane == leader) base = atomicAdd(p.n_cand, __popc(m));
-          base = __shfl_sync(0xFFFFFFFFu, base, leader);
-          if (ok) {
-            uint32_t slot = base + rank;
-            if (slot < p.max_cand) p.cand[slot] = (p.u ? (nl << p.u) : nl) | z;
-            else *p.overflow = 1u;
-          }
-        } else {
-          if (lane == leader) base = atomicAdd(&s_next, __popc(m));
-          base = __shfl_sync(0xFFFFFFFFu, base, leader);
-          if (ok) {
-            uint32_t slot = base + rank;
-            if (slot < p.ws_cap) out[slot] = nl;
-            else *p.overflow = 1u;
-          }
-        }
+      if (!m) continue;
+      const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+      const uint32_t leader = __ffs(m) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(last ? p.n_cand : &s_next, __popc(m));
+      base = __shfl_sync(0xFFFFFFFFu, base, leader);
+      if (!ok) continue;
+      const uint32_t slot = base + rank;
+      if (!last) {
+        if (slot < kPartSmem) s_part[ob][slot] = nl;
+        else if (slot < kPartSmem + p.ws_cap) gbuf[ob][slot - kPartSmem] = nl;
+        else *p.overflow = 1u;
+        continue;
       }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_nin = (uint32_t)min((uint64_t)s_next, p.ws_cap);
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------ NAT + Eq. 5
-
-struct NatParams {
-  const uint32_t* cand;        // mangled values h
-  const uint32_t* active;      // active bits, wpa words per ATV
-  const unsigned long long* aat;
-  void* reports;               // asse_report[n] (ip, nat, estimate, flags, pad)
-  uint32_t* keys;              // ip, for the sort
-  uint32_t* vals;              // index, for the sort
-  uint32_t* n_above;
-  const uint32_t* n_cand;      // |CSIP| (device), clamped to max_cand
-  uint32_t max_cand;
-  uint32_t A_inv, r, u, c, W, F, g, wpa;
-  double theta, cells;         // cells = g * 2^c
-  uint32_t shift[kMaxR];
-};
-
-struct ReportDev { uint32_t ip, nat; double estimate; uint32_t flags, pad; };
-
-// Alg. 5 NAT as an AND of the r active bit rows + popcount, UP (Eq. 4,
-// P:412) from AAT in double, Eq. 5 (A19), flags (A20, A21).
-__global__ void __launch_bounds__(256) k_nat_est(NatParams p) {
-  // LPC lanes per candidate: lane j of a group reads the j-th 16-byte word of each of
-  // the r active rows (independent loads), ANDs them and the group sums popcounts.
-  const uint32_t lpc = p.wpa / 4;                   // 1, 2 or 4 (g = 128, 256, 512)
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t sub = lane & (lpc - 1u);
-  const uint32_t fmask = (1u << p.u) - 1u;
-  const uint32_t cmask = (1u << p.c) - 1u;
-  const uint32_t n = min(*p.n_cand, p.max_cand);
-  const uint32_t groups_per_grid = (gridDim.x * blockDim.x) / lpc;
-  const uint32_t g0 = (blockIdx.x * blockDim.x + threadIdx.x) / lpc;
-  const uint32_t rounds = (n + groups_per_grid - 1) / groups_per_grid;
-  for (uint32_t rd = 0; rd < rounds; ++rd) {
-    const uint32_t q = g0 + rd * groups_per_grid;
-    const bool valid = q < n;
-    uint32_t nat = 0, h = 0, z = 0;
-    if (valid) {
-      h = p.cand[q];
-      z = h & fmask;
-      const uint64_t L = (uint64_t)(h >> p.u);
-      const uint64_t D = L | (L << p.W);
-      uint4 a = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      if (slot >= p.max_cand) { *p.overflow = 1u; continue; }
+      // a restored candidate: f(ip) = (LBS << u) | z, ip = A^{-1} f
+      const uint32_t h = (p.u ? (nl << p.u) : nl) | z;
+      p.cand[slot] = h;
+      // Alg. 5 NAT: ATs active in all r ATVs of the candidate
+      const uint64_t DL = (uint64_t)nl | ((uint64_t)nl << p.W);
+      const uint4* rows[kMaxR];
 #pragma unroll
-      for (int y = 0; y < kMaxR; ++y) {
-        if (y < (int)p.r) {
-          const uint32_t x = (uint32_t)(D >> p.shift[y]) & cmask;
-          const size_t atv = (((size_t)y * p.F + z) << p.c) | x;
-          const uint4 b = __ldcg(reinterpret_cast<const uint4*>(p.active + atv * p.wpa) + sub);
-          a.x &= b.x; a.y &= b.y; a.z &= b.z; a.w &= b.w;
+      for (int yy = 0; yy < kMaxR; ++yy) {
+        if (yy < (int)p.r) {
+          const uint32_t xx = (uint32_t)(DL >> p.shift[yy]) & cmask;
+          rows[yy] = reinterpret_cast<const uint4*>(p.active + ((((size_t)yy * p.F + z) << p.c) | xx) * p.wpa);
         }
       }
-      nat = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
-    }
-    for (uint32_t off = 1; off < lpc; off <<= 1) nat += __shfl_xor_sync(0xFFFFFFFFu, nat, off);
-    if (valid && sub == 0) {
-      double up = 0.0;
-      for (uint32_t y = 0; y < p.r; ++y) {
-        const double P = (double)p.aat[y * p.F + z] / p.cells;   // P_{y,z}^{k'}
-        up = (y == 0) ? P : up * P;                                // UP = prod_y P
+      uint32_t nat = 0;
+      for (uint32_t w4 = 0; w4 < p.wpa / 4; ++w4) {
+        uint4 acc = __ldcg(rows[0] + w4);
+#pragma unroll
+        for (int yy = 1; yy < kMaxR; ++yy) {
+          if (yy < (int)p.r) {
+            const uint4 b4 = __ldcg(rows[yy] + w4);
+            acc.x &= b4.x; acc.y &= b4.y; acc.z &= b4.z; acc.w &= b4.w;
+          }
+        }
+        nat += __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
       }
+      // Eq. 5 (A19) in double; NAT == g -> +inf (A20)
       double est;
-      if (nat == p.g) est = __longlong_as_double(0x7FF0000000000000LL);   // +inf (A20)
-      else est = -(double)p.g * log((double)(p.g - nat) / ((double)p.g * (1.0 - up)));
+      if (nat == p.g) est = __longlong_as_double(0x7FF0000000000000LL);
+      else est = -(double)p.g * log((double)(p.g - nat) / ((double)p.g * (1.0 - s_up)));
       const uint32_t flags = (nat == p.g ? 1u : 0u) | (est >= p.theta ? 2u : 0u);
-      const uint32_t ip = p.A_inv * h;                               // f^{-1}
-      ReportDev* R = reinterpret_cast<ReportDev*>(p.reports) + q;
+      const uint32_t ip = p.A_inv * h;
+      ReportDev* R = reinterpret_cast<ReportDev*>(p.reports) + slot;
       R->ip = ip; R->nat = nat; R->estimate = est; R->flags = flags; R->pad = 0;
-      p.keys[q] = ip;
-      p.vals[q] = q;
+      p.keys[slot] = ip;
+      p.vals[slot] = slot;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) s_nin = (uint32_t)min((uint64_t)s_next, (uint64_t)kPartSmem + p.ws_cap);
+    __syncthreads();
   }
+  pdl_trigger();
 }
 
 // gather reports in ascending-ip order (A24)
@@ -624,17 +604,22 @@ __global__ void k_gather(const ReportDev* __restrict__ in, const uint32_t* __res
     out_all[q] = in[order[q]];
 }
 
-// Sort of a small CSIP by ip (A24) inside one CTA (block radix sort in shared
-// memory), then the ascending-ip report array and its est >= theta subset (A21).
-// If |CSIP| exceeds the block capacity it only raises *big (the host then runs the
-// device-wide radix sort). counters: [0] n_cand, [2] n_above, [4] n_sel, [5] big.
+// Sort of CSIP by ip (A24) and the est >= theta subset (A21), |CSIP| read on the device:
+//  * |CSIP| <= 2048: rank sort, one warp per element — CSIP ips are distinct (tuple <->
+//    LBS bijection, A16), so an element's position is the number of smaller ips and its
+//    position among the ABOVE_THETA reports counts the smaller flagged ips;
+//  * <= 8192: CTA 0 runs a block radix sort;
+//  * larger: counters[5] = 1 and the host runs the device-wide radix sort.
+// counters: [0] n_cand, [4] n_above, [5] big.
 constexpr int kSortThreads = 512;
-constexpr uint32_t kSortCap = kSortThreads * 16;   // 8192
+constexpr uint32_t kRankCap = 2048;
+constexpr int kSortBlocks = kRankCap / (kSortThreads / 32);   // 128: one warp per element
+constexpr uint32_t kSortCap = kSortThreads * 16;               // 8192
 
 template <int ITEMS>
-__device__ __forceinline__ void sort_and_emit(const ReportDev* __restrict__ rep, uint32_t n,
-                                              ReportDev* __restrict__ sorted, ReportDev* __restrict__ above,
-                                              uint32_t* counters, void* tmp_raw, uint32_t* warp_cnt) {
+__device__ __forceinline__ void block_sort_emit(const ReportDev* __restrict__ rep, uint32_t n,
+                                                ReportDev* __restrict__ sorted, ReportDev* __restrict__ above,
+                                                uint32_t* counters, void* tmp_raw, uint32_t* warp_cnt) {
   using BlockSort = cub::BlockRadixSort<uint32_t, kSortThreads, ITEMS, uint32_t, 4>;
   auto& tmp = *reinterpret_cast<typename BlockSort::TempStorage*>(tmp_raw);
   uint32_t keys[ITEMS], idx[ITEMS];
@@ -645,17 +630,14 @@ __device__ __forceinline__ void sort_and_emit(const ReportDev* __restrict__ rep,
     idx[j] = q;
   }
   BlockSort(tmp).Sort(keys, idx);                        // stable, ascending
-  uint32_t mine = 0;
-  uint32_t sel[ITEMS];
+  uint32_t mine = 0, sel = 0;
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const uint32_t q = threadIdx.x * ITEMS + j;
-    sel[j] = 0;
     if (q < n) {
       const ReportDev r = rep[idx[j]];
       sorted[q] = r;
-      sel[j] = (r.flags & 2u) ? 1u : 0u;
-      mine += sel[j];
+      if (r.flags & 2u) { sel |= 1u << j; mine++; }
     }
   }
   // exclusive prefix over threads (thread order == ip order in the blocked layout)
@@ -672,49 +654,58 @@ __device__ __forceinline__ void sort_and_emit(const ReportDev* __restrict__ rep,
     uint32_t acc = 0;
     for (int w = 0; w < kSortThreads / 32; ++w) { const uint32_t t = warp_cnt[w]; warp_cnt[w] = acc; acc += t; }
     counters[4] = acc;
-    counters[5] = 0u;
   }
   __syncthreads();
   uint32_t pos = warp_cnt[wid] + incl - mine;
 #pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const uint32_t q = threadIdx.x * ITEMS + j;
-    if (q < n && sel[j]) above[pos++] = rep[idx[j]];
-  }
+  for (int j = 0; j < ITEMS; ++j)
+    if ((sel >> j) & 1u) above[pos++] = rep[idx[j]];
 }
 
-// Rank sort for |CSIP| <= 2048 (one CTA): CSIP ips are distinct (a tuple <-> LBS
-// bijection, A16), so an element's position is the number of smaller ips; its position
-// among the est >= theta reports counts the smaller ips flagged ABOVE_THETA.
-constexpr int kRankThreads = 256;
-constexpr uint32_t kRankCap = 2048;
-constexpr int kRankBlocks = kRankCap / (kRankThreads / 32);   // one warp per element
-__global__ void __launch_bounds__(kRankThreads) k_rank_sort(const ReportDev* __restrict__ rep,
-                                                            uint32_t* counters, uint32_t max_cand,
-                                                            ReportDev* __restrict__ sorted,
-                                                            ReportDev* __restrict__ above) {
-  __shared__ uint32_t s_key[kRankCap];
-  __shared__ uint32_t s_above[kRankCap / 32];   // ABOVE_THETA flags as a bitset
+__global__ void __launch_bounds__(kSortThreads) k_sort(const ReportDev* __restrict__ rep, uint32_t* counters,
+                                                       uint32_t max_cand, ReportDev* __restrict__ sorted,
+                                                       ReportDev* __restrict__ above) {
+  using S16 = cub::BlockRadixSort<uint32_t, kSortThreads, 16, uint32_t, 4>;
+  union Smem {
+    typename S16::TempStorage radix;                   // the largest block-sort instance
+    struct { uint32_t key[kRankCap]; uint32_t above[kRankCap / 32]; } rank;
+  };
+  __shared__ __align__(16) Smem sm;
+  __shared__ uint32_t warp_cnt[kSortThreads / 32];
+  pdl_wait();                                          // k_restore's reports and |CSIP|
   const uint32_t n = min(counters[0], max_cand);
-  if (n > kRankCap || n == 0) return;
-  const uint32_t q = blockIdx.x * (kRankThreads / 32) + (threadIdx.x >> 5);
-  if (blockIdx.x * (kRankThreads / 32) >= n) return;       // CTA without elements
-  for (uint32_t j = threadIdx.x; j < kRankCap / 32; j += kRankThreads) s_above[j] = 0;
+  if (n == 0) return;
+  if (n > kSortCap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) counters[5] = 1u;
+    return;
+  }
+  if (n > kRankCap) {
+    if (blockIdx.x != 0) return;
+    if (n <= kSortThreads * 4) block_sort_emit<4>(rep, n, sorted, above, counters, &sm.radix, warp_cnt);
+    else if (n <= kSortThreads * 8) block_sort_emit<8>(rep, n, sorted, above, counters, &sm.radix, warp_cnt);
+    else block_sort_emit<16>(rep, n, sorted, above, counters, &sm.radix, warp_cnt);
+    return;
+  }
+  // rank sort
+  const uint32_t first = blockIdx.x * (kSortThreads / 32);
+  if (first >= n) return;                              // CTA without elements
+  for (uint32_t j = threadIdx.x; j < kRankCap / 32; j += kSortThreads) sm.rank.above[j] = 0;
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < n; j += kRankThreads) {
+  for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
     const ReportDev r = rep[j];
-    s_key[j] = r.ip;
-    if (r.flags & 2u) atomicOr(&s_above[j >> 5], 1u << (j & 31u));
+    sm.rank.key[j] = r.ip;
+    if (r.flags & 2u) atomicOr(&sm.rank.above[j >> 5], 1u << (j & 31u));
   }
   __syncthreads();
+  const uint32_t q = first + (threadIdx.x >> 5);
   if (q >= n) return;
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t k = s_key[q];
+  const uint32_t k = sm.rank.key[q];
   uint32_t r_all = 0, r_above = 0;
   for (uint32_t j = lane; j < n; j += 32) {
-    const uint32_t less = s_key[j] < k ? 1u : 0u;
+    const uint32_t less = sm.rank.key[j] < k ? 1u : 0u;
     r_all += less;
-    r_above += less & (s_above[j >> 5] >> (j & 31u));
+    r_above += less & (sm.rank.above[j >> 5] >> (j & 31u));
   }
   r_all = __reduce_add_sync(0xFFFFFFFFu, r_all);
   r_above = __reduce_add_sync(0xFFFFFFFFu, r_above);
@@ -726,30 +717,6 @@ __global__ void __launch_bounds__(kRankThreads) k_rank_sort(const ReportDev* __r
       atomicAdd(counters + 4, 1u);
     }
   }
-}
-
-// Sort of a small CSIP by ip (A24) inside one CTA (block radix sort, 4-bit digits, item
-// count picked from |CSIP| read on the device), then the ascending-ip report array and
-// its est >= theta subset (A21). If |CSIP| exceeds the block capacity it only raises
-// counters[5] and the host runs the device-wide radix sort.
-// counters: [0] n_cand, [4] n_above, [5] big.
-__global__ void __launch_bounds__(kSortThreads) k_sort_small(const ReportDev* __restrict__ rep,
-                                                             uint32_t* counters, uint32_t max_cand,
-                                                             ReportDev* __restrict__ sorted,
-                                                             ReportDev* __restrict__ above) {
-  using S16 = cub::BlockRadixSort<uint32_t, kSortThreads, 16, uint32_t, 4>;
-  __shared__ __align__(16) typename S16::TempStorage tmp;   // the largest instance
-  __shared__ uint32_t warp_cnt[kSortThreads / 32];
-  const uint32_t n = min(counters[0], max_cand);
-  if (n <= kRankCap) return;                                 // k_rank_sort's case
-  if (n > kSortCap) {
-    if (threadIdx.x == 0) counters[5] = 1u;
-    return;
-  }
-  if (n <= kSortThreads * 2) sort_and_emit<2>(rep, n, sorted, above, counters, &tmp, warp_cnt);
-  else if (n <= kSortThreads * 4) sort_and_emit<4>(rep, n, sorted, above, counters, &tmp, warp_cnt);
-  else if (n <= kSortThreads * 8) sort_and_emit<8>(rep, n, sorted, above, counters, &tmp, warp_cnt);
-  else sort_and_emit<16>(rep, n, sorted, above, counters, &tmp, warp_cnt);
 }
 
 // --------------------------------------------------------------- export
