@@ -130,6 +130,20 @@ def oracle_sample(p, pk_host, n_slice, reps=1):
     return n_slice / per_slice / 1e9, dict(scan_s=scan_s, end_s=end_s, sample_packets=len(pk_host))
 
 
+def workload_config(args, p, n_slice, world, S=None):
+    """The `config` object of the JSON line (identical for both arms)."""
+    cfg = {"workload": "%s: config-3 mixture, %d packets/slice split round-robin over %d GPU(s)"
+                       % (args.workload, n_slice, world),
+           "packets_per_slice": n_slice, "k": p["k"], "theta": p["theta"],
+           "sketch": "r=%d x 2^(c+u)=%d x g=%d (c=%d u=%d s=%d)" % (
+               p["r"], 1 << (p["c"] + p["u"]), p["g"], p["c"], p["u"], p["s"]),
+           "parallelism": "dp%d" % world,
+           "l2": "inputs larger than L2 (%d MB per slice per GPU), no flush" % (8 * n_slice // world >> 20)}
+    if S is not None:
+        cfg["distinct_slices"] = S
+    return cfg
+
+
 def bench_reference(args, p, n_slice):
     """--impl reference: the CPU oracle as it stands, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
@@ -156,7 +170,7 @@ def bench_reference(args, p, n_slice):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-        "config": {"workload": args.workload, "packets_per_slice": n_slice},
+        "config": workload_config(args, p, n_slice, args.gpus),
         "cpu_baseline": {"value": value, "unit": "Gpps", "cores": 1, "kind": "oracle",
                          "sample": "per step: first %d packets of slice t scanned, full end_slice "
                                    "at the full geometry; scan time projected to %d packets"
@@ -307,13 +321,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8" if cb == 1 else "u16",
             "data": "synthetic",
-            "config": {"workload": "%s: config-3 mixture, %d packets/slice split round-robin over %d GPU(s)"
-                                   % (args.workload, n_slice, world),
-                       "packets_per_slice": n_slice, "k": p["k"], "theta": p["theta"],
-                       "sketch": "r=%d x 2^(c+u)=%d x g=%d (c=%d u=%d s=%d)" % (
-                           p["r"], 1 << (p["c"] + p["u"]), p["g"], p["c"], p["u"], p["s"]),
-                       "distinct_slices": S, "parallelism": "dp%d" % world,
-                       "l2": "inputs larger than L2 (%d MB per slice per GPU), no flush" % (8 * n_local >> 20)},
+            "config": workload_config(args, p, n_slice, world, S),
             "end_slice_ms": statistics.mean(end_ms),
             "end_slice_ms_max": max(end_ms),
             "end_slice_breakdown_ms": {k[5:-3]: statistics.mean(v) for k, v in phases.items()},

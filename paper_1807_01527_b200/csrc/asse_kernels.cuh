@@ -759,6 +759,9 @@ __global__ void __launch_bounds__(256) k_merge_or(MergeParams p) {
     }
     for (uint32_t w = 0; w < p.world; ++w) __stcg(p.merged[w] + q, acc);
   }
+  // make this thread's peer stores visible system-wide before the kernel completes;
+  // the following k_barrier release/acquire then orders them before every rank's fold
+  __threadfence_system();
 }
 
 struct BarrierParams {

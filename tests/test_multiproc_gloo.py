@@ -79,3 +79,18 @@ def test_gloo_world2_sharded_pools_merge_to_single():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+@pytest.mark.parametrize("n,world", [(0, 1), (1, 2), (7, 2), (100_000_000, 8), (200_001, 3)])
+def test_shard_slots_partition(n, world):
+    """Round-robin sharding covers every slot exactly once (BASELINE.json.configs[4])."""
+    from paper_1807_01527_b200.dist import shard_slots
+    seen = []
+    for r in range(world):
+        j0, stride, m = shard_slots(n, r, world)
+        assert stride == world and j0 == r
+        if n <= 10_000_000:
+            seen.extend(range(j0, n, stride)[:m])
+        assert m == len(range(j0, n, stride))
+    if n <= 10_000_000:
+        assert sorted(seen) == list(range(n))
