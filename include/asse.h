@@ -127,6 +127,16 @@ asse_status asse_scan_slice_host(void* ctx, const uint32_t* h_pairs, uint64_t n_
 asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out,
                            uint32_t mode);
 
+/* Window query (checkAT for any k' <= k): super
+ * points and Eq. 5 estimates over the k_prime slices ending at the last closed slice,
+ * evaluated on the current pool without modifying it. 1 <= k_prime < k (the advance's
+ * preserveAT has erased ages >= k-1 of that slice, which only the k' = k window uses;
+ * k' = k is what asse_end_slice returns with k_prime = 0). Needs >= 1 closed slice;
+ * pending scans of the next slice are ignored. Same output conventions as
+ * asse_end_slice; afterwards asse_fetch_reports returns this query's reports. */
+asse_status asse_query_window(void* ctx, uint32_t k_prime, asse_report* h_out, uint32_t cap,
+                              uint32_t* n_out, uint32_t mode);
+
 /* Re-read the reports of the last closed slice (same mode semantics). */
 asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out,
                                uint32_t mode);
@@ -136,6 +146,16 @@ asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint
  * n must equal r * 2^u * 2^c * g. Reflects the state after the last end_slice
  * (post-advance, A32) plus any scans issued since (not yet folded: excluded). */
 asse_status asse_export_pool(void* ctx, uint16_t* h_out, uint64_t n);
+
+/* Checkpoint: write the pool codes, slice index t and ACT
+ * base C0 with the parameters (k, k', r, c, u, s, g, theta, seed) and a magic/version
+ * header to `path`. Take it after asse_end_slice (touches of a slice still being
+ * scanned are not saved). ASSE_E_PARAM on I/O errors. */
+asse_status asse_save_state(void* ctx, const char* path);
+
+/* Restore a checkpoint into a context created with the same parameters (rejects any
+ * mismatch with ASSE_E_PARAM); pending touches of the context are discarded. */
+asse_status asse_load_state(void* ctx, const char* path);
 
 /* Number of ATs in the pool (r * 2^u * 2^c * g). */
 uint64_t asse_pool_size(const void* ctx);

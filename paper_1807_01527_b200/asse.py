@@ -25,7 +25,7 @@ SYMBOLS = ["asse_validate", "asse_init", "asse_destroy", "asse_last_error", "ass
            "asse_scan_slice", "asse_scan_slice_host", "asse_end_slice", "asse_fetch_reports",
            "asse_export_pool", "asse_pool_size", "asse_get_clock", "asse_get_keys",
            "asse_get_stats", "asse_get_stream", "asse_attach_peers", "asse_bitmap_bytes",
-           "asse_merge"]
+           "asse_merge", "asse_query_window", "asse_save_state", "asse_load_state"]
 
 
 class AsseError(RuntimeError):
@@ -91,6 +91,9 @@ def load_library(path=LIB_PATH):
         "asse_attach_peers": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), u32]),
         "asse_bitmap_bytes": (u64, [vp]),
         "asse_merge": (i32, [vp]),
+        "asse_query_window": (i32, [vp, u32, vp, u32, ctypes.POINTER(u32), u32]),
+        "asse_save_state": (i32, [vp, ctypes.c_char_p]),
+        "asse_load_state": (i32, [vp, ctypes.c_char_p]),
     }
     for name, (rt, at) in sigs.items():
         f = getattr(L, name)
@@ -185,6 +188,17 @@ class Asse:
         self._check(st)
         return self._buf[:n.value].copy()
 
+    def query_window(self, k_prime, mode=1):
+        """Reports of the window of k_prime < k slices ending at the last closed slice."""
+        n = ctypes.c_uint32()
+        self._ensure(1)
+        st = self._L.asse_query_window(self._h, k_prime, self._buf.ctypes.data, self._cap,
+                                       ctypes.byref(n), mode)
+        if st == E_CAPACITY:
+            return self.fetch_reports(mode)
+        self._check(st)
+        return self._buf[:n.value].copy()
+
     def fetch_reports(self, mode=1):
         n = ctypes.c_uint32()
         st = self._L.asse_fetch_reports(self._h, None, 0, ctypes.byref(n), mode)
@@ -200,6 +214,12 @@ class Asse:
         out = np.empty(n, dtype=np.uint16)
         self._check(self._L.asse_export_pool(self._h, out.ctypes.data, n))
         return out.reshape(self.r, self.F, self.E, self.g)
+
+    def save_state(self, path):
+        self._check(self._L.asse_save_state(self._h, os.fsencode(path)))
+
+    def load_state(self, path):
+        self._check(self._L.asse_load_state(self._h, os.fsencode(path)))
 
     def clock(self):
         t, c0 = ctypes.c_uint64(), ctypes.c_uint32()

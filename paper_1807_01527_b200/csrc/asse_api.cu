@@ -180,20 +180,23 @@ static void free_all(Ctx* c) {
 
 template <int CB, int LPAL>
 static cudaError_t fold_occ_t(int* occ) {
-  cudaError_t e = cudaFuncSetAttribute(k_fold<CB, LPAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_fold<CB, LPAL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)fold_smem<CB>());
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_fold<CB, LPAL>, kFoldThreads, fold_smem<CB>());
+  e = cudaFuncSetAttribute(k_fold<CB, LPAL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)fold_smem<CB>());
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_fold<CB, LPAL, false>, kFoldThreads, fold_smem<CB>());
 }
 static cudaError_t fold_occupancy(uint32_t cb, uint32_t lpal, int* occ) {
   if (cb == 1) return lpal == 3 ? fold_occ_t<1, 3>(occ) : lpal == 4 ? fold_occ_t<1, 4>(occ) : fold_occ_t<1, 5>(occ);
   return lpal == 3 ? fold_occ_t<2, 3>(occ) : lpal == 4 ? fold_occ_t<2, 4>(occ) : fold_occ_t<2, 5>(occ);
 }
-template <int CB>
+template <int CB, bool WEIGH = false>
 static void launch_fold(uint32_t lpal, unsigned blocks, cudaStream_t s, const FoldParams& fp) {
-  if (lpal == 3) k_fold<CB, 3><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
-  else if (lpal == 4) k_fold<CB, 4><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
-  else k_fold<CB, 5><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
+  if (lpal == 3) k_fold<CB, 3, WEIGH><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
+  else if (lpal == 4) k_fold<CB, 4, WEIGH><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
+  else k_fold<CB, 5, WEIGH><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
 }
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while the
@@ -594,6 +597,46 @@ static asse_status copy_reports(Ctx* c, asse_report* h_out, uint32_t cap, uint32
   return ASSE_OK;
 }
 
+// a7 + a8: restore (Alg. 4, parts CTAs per frame) with NAT and Eq. 5 fused, then the
+// sort by ip; both are launched with programmatic dependent launch so their launch
+// overlaps the previous kernel's tail (griddepcontrol.wait inside).
+static asse_status enqueue_tail(Ctx* c) {
+  const asse_config& p = c->cfg;
+  cudaStream_t s = c->stream;
+  RestoreParams rp = c->rp0;
+  rp.sa_cnt = c->sa_cnt; rp.sa_list = c->sa_list; rp.sa_bits = c->sa_bits;
+  rp.ws = c->ws; rp.ws_cap = c->ws_cap;
+  rp.cand = c->cand; rp.n_cand = c->counters + 0; rp.overflow = c->counters + 1;
+  rp.active = c->active; rp.aat = c->aat; rp.reports = c->rep; rp.keys = c->keys; rp.vals = c->vals;
+  CK(launch_pdl(k_restore, dim3(c->F * rp.parts), dim3(512), c->restore_smem, s, rp));
+  CK(launch_pdl(k_sort, dim3(kSortBlocks), dim3(kSortThreads), 0, s, (const ReportDev*)c->rep, c->counters,
+                (uint32_t)p.max_candidates, c->rep_sorted, c->rep_above));
+  return ASSE_OK;
+}
+
+static FoldParams fold_params(Ctx* c, const uint32_t* src, uint32_t kp) {
+  const asse_config& p = c->cfg;
+  FoldParams fp{};
+  fp.pool = c->pool;
+  fp.touch_src = src;
+  fp.touch_zero = c->touch;
+  fp.active = c->active;
+  fp.aat = c->aat;
+  fp.sa_cnt = c->sa_cnt;
+  fp.sa_list = c->sa_list;
+  fp.sa_bits = c->sa_bits;
+  fp.n_super = c->counters + 3;
+  fp.n_chunks = c->n_at / 512;
+  fp.C0 = c->d_clock;
+  fp.g = p.g; fp.k = p.k; fp.kp = kp; fp.a = c->a;
+  fp.c = p.c; fp.w_theta = c->w_theta; fp.lpa_log2 = c->lpa_log2;
+  return fp;
+}
+static unsigned fold_blocks(const Ctx* c) {
+  const uint64_t tiles = (c->n_at / 512 + kFoldChunksPerTile - 1) / kFoldChunksPerTile;
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)c->fold_grid));
+}
+
 // Every device operation of end_slice up to the result copies, in stream order. Used
 // eagerly (world > 1 with a device barrier) or captured once into a CUDA graph per
 // (timing, mode) and replayed every slice; the per-slice ACT base comes from d_clock.
@@ -621,45 +664,103 @@ static asse_status enqueue_end_slice(Ctx* c, uint32_t mode, bool timing, bool ca
   // a6: fold + weights + super + preserve(t+1)
   CK(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, s));   // AAT, SA counts/bits, counters
   {
-    FoldParams fp{};
-    fp.pool = c->pool;
-    fp.touch_src = src;
-    fp.touch_zero = c->touch;
-    fp.active = c->active;
-    fp.aat = c->aat;
-    fp.sa_cnt = c->sa_cnt;
-    fp.sa_list = c->sa_list;
-    fp.sa_bits = c->sa_bits;
-    fp.n_super = c->counters + 3;
-    fp.n_chunks = c->n_at / 512;
-    fp.C0 = c->d_clock;
-    fp.g = p.g; fp.k = p.k; fp.kp = c->kp; fp.a = c->a;
-    fp.c = p.c; fp.w_theta = c->w_theta; fp.lpa_log2 = c->lpa_log2;
-    const uint64_t tiles = (fp.n_chunks + kFoldChunksPerTile - 1) / kFoldChunksPerTile;
-    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)c->fold_grid));
+    const FoldParams fp = fold_params(c, src, c->kp);
     if (timing) CK(rec(2));
-    if (c->cb == 1) launch_fold<1>(c->lpa_log2, (unsigned)blocks, s, fp);
-    else launch_fold<2>(c->lpa_log2, (unsigned)blocks, s, fp);
+    if (c->cb == 1) launch_fold<1>(c->lpa_log2, fold_blocks(c), s, fp);
+    else launch_fold<2>(c->lpa_log2, fold_blocks(c), s, fp);
     CK(cudaGetLastError());
     if (timing) CK(rec(3));
   }
-  // a7 + a8: restore (Alg. 4, parts CTAs per frame) with NAT and Eq. 5 fused, then the
-  // sort by ip; both are launched with programmatic dependent launch so their launch
-  // overlaps the previous kernel's tail (griddepcontrol.wait inside).
   {
-    RestoreParams rp = c->rp0;
-    rp.sa_cnt = c->sa_cnt; rp.sa_list = c->sa_list; rp.sa_bits = c->sa_bits;
-    rp.ws = c->ws; rp.ws_cap = c->ws_cap;
-    rp.cand = c->cand; rp.n_cand = c->counters + 0; rp.overflow = c->counters + 1;
-    rp.active = c->active; rp.aat = c->aat; rp.reports = c->rep; rp.keys = c->keys; rp.vals = c->vals;
-    CK(launch_pdl(k_restore, dim3(c->F * rp.parts), dim3(512), c->restore_smem, s, rp));
+    asse_status st = enqueue_tail(c);
+    if (st != ASSE_OK) return st;
   }
-  CK(launch_pdl(k_sort, dim3(kSortBlocks), dim3(kSortThreads), 0, s, (const ReportDev*)c->rep, c->counters,
-                (uint32_t)p.max_candidates, c->rep_sorted, c->rep_above));
   if (timing) CK(rec(8));
   return ASSE_OK;
 }
 static constexpr int kEndSliceKernels = 3;   // fold, restore (+NAT), sort
+
+// Copies the counters and a K-report prefix, synchronises once, runs the device-wide
+// sort when |CSIP| exceeds the block sort, records statistics, advances the clock
+// when closing a slice (a9), and hands the reports to the caller.
+static asse_status collect(Ctx* c, uint32_t mode, uint32_t K, asse_report* h_out, uint32_t cap,
+                           uint32_t* n_out, bool advance) {
+  const asse_config& p = c->cfg;
+  cudaStream_t s = c->stream;
+  // results: counters plus a prefix of the requested report array, one synchronisation
+  CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(c->h_rep, mode ? c->rep_sorted : c->rep_above, (size_t)K * sizeof(ReportDev),
+                     cudaMemcpyDeviceToHost, s));
+  if (c->timing && advance) CK(cudaEventRecord(c->ev[9], s));
+  if (advance) {
+    c->stats.kernel_launches += kEndSliceKernels + (c->peers && c->sync_mode == 0 ? 3 : 0);
+    c->stats.fold_launches++;
+  }
+  CK(cudaStreamSynchronize(s));
+  const uint32_t n_cand_raw = c->h_counters[0];
+  const bool overflow = c->h_counters[1] != 0 || n_cand_raw > p.max_candidates;
+  const uint32_t n_cand = overflow ? 0 : n_cand_raw;
+  bool prefetched = true;
+  if (!overflow && c->h_counters[5]) {
+    // |CSIP| above the block-sort capacity: device-wide radix sort (needs n on the host)
+    cub::DoubleBuffer<uint32_t> dk(c->keys, c->keys_alt), dv(c->vals, c->vals_alt);
+    size_t bytes = c->cub_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, dk, dv, (int)n_cand, 0, 32, s));
+    c->stats.kernel_launches += 4;  // onesweep radix passes (count is indicative)
+    unsigned blocks = (unsigned)std::min<uint64_t>((n_cand + 255) / 256, (uint64_t)c->sms * 8);
+    k_gather<<<blocks, 256, 0, s>>>(c->rep, dv.Current(), n_cand, c->rep_sorted);
+    CK(cudaGetLastError());
+    LAUNCHED(c);
+    bytes = c->cub_bytes;
+    CK(cub::DeviceSelect::If(c->cub_tmp, bytes, c->rep_sorted, c->rep_above, c->counters + 4,
+                             (int)n_cand, AboveTheta(), s));
+    c->stats.kernel_launches += 2;
+    CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    prefetched = false;
+  }
+  c->last_n = n_cand;
+  c->last_above = n_cand ? c->h_counters[4] : 0;
+  c->have_reports = true;
+  c->stats.last_n_super = c->h_counters[3];
+  c->stats.last_n_candidates = n_cand_raw;
+  c->stats.last_n_above = c->last_above;
+  if (c->timing && advance) {
+    float ms;
+    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1])); c->stats.last_merge_ms = ms;
+    CK(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3])); c->stats.last_fold_ms = ms;
+    c->stats.fold_ms_total += ms;
+    // restore + NAT + sort run back to back under programmatic dependent launch
+    CK(cudaEventElapsedTime(&ms, c->ev[3], c->ev[8])); c->stats.last_restore_ms = ms;
+    c->stats.last_nat_ms = 0;
+    c->stats.last_sort_ms = 0;
+    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[9])); c->stats.last_end_slice_ms = ms;
+    asse_status hs = harvest_scan_timing(c);
+    if (hs != ASSE_OK) return hs;
+  }
+  if (advance) {
+    // a9: advance; preserveAT for t+1 already applied by k_fold (Alg. 2)
+    c->t += 1;
+    c->C0 = (uint32_t)(c->t % c->two_k);
+    c->stats.slices_closed++;
+  }
+  if (overflow) {
+    c->last_n = c->last_above = 0;
+    c->err = "CSIP exceeded max_candidates (or the restore join workspace)";
+    return ASSE_E_OVERFLOW;
+  }
+  const uint32_t n = mode ? c->last_n : c->last_above;
+  if (prefetched && n <= K) {
+    if (n_out) *n_out = n;
+    if (!h_out) return n > cap ? ASSE_E_CAPACITY : ASSE_OK;
+    if (n > cap) return ASSE_E_CAPACITY;
+    memcpy(h_out, c->h_rep, (size_t)n * sizeof(ReportDev));
+    return ASSE_OK;
+  }
+  return copy_reports(c, h_out, cap, n_out, mode);
+}
+
+
 
 asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
   if (!ctx) return ASSE_E_PARAM;
@@ -694,73 +795,36 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
     }
     CK(cudaGraphLaunch(ge, s));
   }
-  // results: counters plus a prefix of the requested report array, one synchronisation
-  CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(c->h_rep, mode ? c->rep_sorted : c->rep_above, (size_t)K * sizeof(ReportDev),
-                     cudaMemcpyDeviceToHost, s));
-  if (timing) CK(cudaEventRecord(c->ev[9], s));
-  c->stats.kernel_launches += kEndSliceKernels + (c->peers && c->sync_mode == 0 ? 3 : 0);
-  c->stats.fold_launches++;
-  CK(cudaStreamSynchronize(s));
-  const uint32_t n_cand_raw = c->h_counters[0];
-  const bool overflow = c->h_counters[1] != 0 || n_cand_raw > p.max_candidates;
-  const uint32_t n_cand = overflow ? 0 : n_cand_raw;
-  bool prefetched = true;
-  if (!overflow && c->h_counters[5]) {
-    // |CSIP| above the block-sort capacity: device-wide radix sort (needs n on the host)
-    cub::DoubleBuffer<uint32_t> dk(c->keys, c->keys_alt), dv(c->vals, c->vals_alt);
-    size_t bytes = c->cub_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, dk, dv, (int)n_cand, 0, 32, s));
-    c->stats.kernel_launches += 4;  // onesweep radix passes (count is indicative)
-    unsigned blocks = (unsigned)std::min<uint64_t>((n_cand + 255) / 256, (uint64_t)c->sms * 8);
-    k_gather<<<blocks, 256, 0, s>>>(c->rep, dv.Current(), n_cand, c->rep_sorted);
-    CK(cudaGetLastError());
-    LAUNCHED(c);
-    bytes = c->cub_bytes;
-    CK(cub::DeviceSelect::If(c->cub_tmp, bytes, c->rep_sorted, c->rep_above, c->counters + 4,
-                             (int)n_cand, AboveTheta(), s));
-    c->stats.kernel_launches += 2;
-    CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    prefetched = false;
-  }
-  c->last_n = n_cand;
-  c->last_above = n_cand ? c->h_counters[4] : 0;
-  c->have_reports = true;
-  c->stats.last_n_super = c->h_counters[3];
-  c->stats.last_n_candidates = n_cand_raw;
-  c->stats.last_n_above = c->last_above;
-  if (c->timing) {
-    float ms;
-    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1])); c->stats.last_merge_ms = ms;
-    CK(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3])); c->stats.last_fold_ms = ms;
-    c->stats.fold_ms_total += ms;
-    // restore + NAT + sort run back to back under programmatic dependent launch
-    CK(cudaEventElapsedTime(&ms, c->ev[3], c->ev[8])); c->stats.last_restore_ms = ms;
-    c->stats.last_nat_ms = 0;
-    c->stats.last_sort_ms = 0;
-    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[9])); c->stats.last_end_slice_ms = ms;
-    asse_status hs = harvest_scan_timing(c);
-    if (hs != ASSE_OK) return hs;
-  }
-  // a9: advance; preserveAT for t+1 already applied by k_fold (Alg. 2)
-  c->t += 1;
-  c->C0 = (uint32_t)(c->t % c->two_k);
-  c->stats.slices_closed++;
-  if (overflow) {
-    c->last_n = c->last_above = 0;
-    c->err = "CSIP exceeded max_candidates (or the restore join workspace)";
-    return ASSE_E_OVERFLOW;
-  }
-  const uint32_t n = mode ? c->last_n : c->last_above;
-  if (prefetched && n <= K) {
-    if (n_out) *n_out = n;
-    if (!h_out) return n > cap ? ASSE_E_CAPACITY : ASSE_OK;
-    if (n > cap) return ASSE_E_CAPACITY;
-    memcpy(h_out, c->h_rep, (size_t)n * sizeof(ReportDev));
-    return ASSE_OK;
-  }
-  return copy_reports(c, h_out, cap, n_out, mode);
+  return collect(c, mode, K, h_out, cap, n_out, true);
+}
+
+// Window query for k' < k on the closed pool (checkAT for any
+// k' <= k): weights, super ATVs, restore, NAT and Eq. 5 of the window of
+// the k' slices ending at the last closed slice. The pool is not modified; preserveAT
+// of the advance only erased ages >= k-1 of that slice, which no k' < k window uses.
+asse_status asse_query_window(void* ctx, uint32_t k_prime, asse_report* h_out, uint32_t cap,
+                              uint32_t* n_out, uint32_t mode) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (n_out) *n_out = 0;
+  if (mode > 1) { c->err = "mode must be 0 or 1"; return ASSE_E_PARAM; }
+  if (k_prime < 1 || k_prime >= c->cfg.k) { c->err = "query window needs 1 <= k' < k"; return ASSE_E_PARAM; }
+  if (c->t == 0) { c->err = "no closed slice"; return ASSE_E_STATE; }
+  CK(cudaSetDevice(c->device));
+  const asse_config& p = c->cfg;
+  cudaStream_t s = c->stream;
+  const uint32_t K = (uint32_t)std::min<uint64_t>(c->h_rep_cap, p.max_candidates);
+  *c->h_clock = (c->C0 + c->two_k - 1) % c->two_k;          // ACT base of the last closed slice
+  CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, s));
+  const FoldParams fp = fold_params(c, nullptr, k_prime);
+  if (c->cb == 1) launch_fold<1, true>(c->lpa_log2, fold_blocks(c), s, fp);
+  else launch_fold<2, true>(c->lpa_log2, fold_blocks(c), s, fp);
+  CK(cudaGetLastError());
+  asse_status st = enqueue_tail(c);
+  if (st != ASSE_OK) return st;
+  c->stats.kernel_launches += 3;
+  return collect(c, mode, K, h_out, cap, n_out, false);
 }
 
 asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
@@ -770,6 +834,68 @@ asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint
   if (mode > 1) return ASSE_E_PARAM;
   CK(cudaSetDevice(c->device));
   return copy_reports(c, h_out, cap, n_out, mode);
+}
+
+// ------------------------------------------------------------ checkpoint
+// File: "ASSECKPT" | u32 version | u32 code_bytes | u32 k, k', r, c, u, s, g | f64 theta |
+//       u64 seed | u64 t | u32 C0 | u32 pad | pool codes (n_at * code_bytes, canonical values)
+struct CkptHeader {
+  char magic[8];
+  uint32_t version, code_bytes;
+  uint32_t k, kp, r, c, u, s, g;
+  uint32_t pad0;
+  double theta;
+  uint64_t seed, t;
+  uint32_t C0, pad1;
+};
+
+asse_status asse_save_state(void* ctx, const char* path) {
+  if (!ctx || !path) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  CK(cudaSetDevice(c->device));
+  CkptHeader h{};
+  memcpy(h.magic, "ASSECKPT", 8);
+  h.version = 1; h.code_bytes = c->cb;
+  h.k = c->cfg.k; h.kp = c->kp; h.r = c->cfg.r; h.c = c->cfg.c; h.u = c->cfg.u; h.s = c->cfg.s;
+  h.g = c->cfg.g; h.theta = c->cfg.theta; h.seed = c->cfg.seed; h.t = c->t; h.C0 = c->C0;
+  std::vector<uint8_t> buf(c->n_at * c->cb);
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(buf.data(), c->pool, buf.size(), cudaMemcpyDeviceToHost));
+  FILE* f = fopen(path, "wb");
+  if (!f) { c->err = std::string("cannot open ") + path; return ASSE_E_PARAM; }
+  bool ok = fwrite(&h, sizeof(h), 1, f) == 1 && fwrite(buf.data(), 1, buf.size(), f) == buf.size();
+  ok = (fclose(f) == 0) && ok;
+  if (!ok) { c->err = std::string("short write to ") + path; return ASSE_E_PARAM; }
+  return ASSE_OK;
+}
+
+asse_status asse_load_state(void* ctx, const char* path) {
+  if (!ctx || !path) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  CK(cudaSetDevice(c->device));
+  FILE* f = fopen(path, "rb");
+  if (!f) { c->err = std::string("cannot open ") + path; return ASSE_E_PARAM; }
+  CkptHeader h{};
+  std::vector<uint8_t> buf(c->n_at * c->cb);
+  bool ok = fread(&h, sizeof(h), 1, f) == 1;
+  if (ok && (memcmp(h.magic, "ASSECKPT", 8) != 0 || h.version != 1)) { fclose(f); c->err = "not an ASSE checkpoint (v1)"; return ASSE_E_PARAM; }
+  if (ok && (h.code_bytes != c->cb || h.k != c->cfg.k || h.kp != c->kp || h.r != c->cfg.r || h.c != c->cfg.c ||
+             h.u != c->cfg.u || h.s != c->cfg.s || h.g != c->cfg.g || h.theta != c->cfg.theta ||
+             h.seed != c->cfg.seed)) {
+    fclose(f);
+    c->err = "checkpoint parameters differ from the context (k, k', r, c, u, s, g, theta, seed)";
+    return ASSE_E_PARAM;
+  }
+  ok = ok && fread(buf.data(), 1, buf.size(), f) == buf.size();
+  fclose(f);
+  if (!ok) { c->err = std::string("short read from ") + path; return ASSE_E_PARAM; }
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(c->pool, buf.data(), buf.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemset(c->touch, 0, c->n_atv * c->wpa * 4));
+  c->t = h.t;
+  c->C0 = h.C0;
+  c->have_reports = false;
+  return ASSE_OK;
 }
 
 uint64_t asse_pool_size(const void* ctx) {

@@ -233,7 +233,9 @@ template <int CB> constexpr uint32_t fold_code_bytes() { return kFoldChunksPerTi
 template <int CB> constexpr uint32_t fold_stage_bytes() { return fold_code_bytes<CB>() + kFoldChunksPerTile * 64u; }
 template <int CB> constexpr size_t fold_smem() { return (size_t)kFoldStages * fold_stage_bytes<CB>(); }
 
-template <int CB, int LPAL>   // LPAL = log2(lanes per ATV) = log2(g/16): 3, 4 or 5
+// WEIGH = true: read-only variant for window queries with k' < k on the closed pool
+// (SURVEY §8(f) row 1): no touch fold, no preserveAT, no pool write-back.
+template <int CB, int LPAL, bool WEIGH = false>   // LPAL = log2(lanes per ATV) = log2(g/16): 3, 4 or 5
 __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
   using S = Swar<CB>;
   constexpr int NW = S::NW, EPW = S::EPW, EB = S::EB;
@@ -270,11 +272,12 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
         const uint32_t tile = t0 + i;
         const uint32_t nch = (uint32_t)umin64(kFoldChunksPerTile, p.n_chunks - (uint64_t)tile * kFoldChunksPerTile);
         uint8_t* dst = smem + (size_t)st * STAGE_BYTES;
-        mbar_expect_tx(&full[st], nch * (512u * CB + 64u));
+        mbar_expect_tx(&full[st], nch * (512u * CB + (WEIGH ? 0u : 64u)));
         bulk_g2s(dst, reinterpret_cast<const uint8_t*>(p.pool) + (size_t)tile * CODE_BYTES, nch * 512u * CB,
                  &full[st], pol);
-        bulk_g2s(dst + CODE_BYTES, p.touch_src + (size_t)tile * kFoldChunksPerTile * 16u, nch * 64u,
-                 &full[st], keep);
+        if (!WEIGH)
+          bulk_g2s(dst + CODE_BYTES, p.touch_src + (size_t)tile * kFoldChunksPerTile * 16u, nch * 64u,
+                   &full[st], keep);
       }
     }
     return;
@@ -345,7 +348,7 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
         const uint4 t4 = scodes[cc * (32u * LW / 4) + v4];
         cur[4 * v4 + 0] = t4.x; cur[4 * v4 + 1] = t4.y; cur[4 * v4 + 2] = t4.z; cur[4 * v4 + 3] = t4.w;
       }
-      const uint32_t field = (stouch[cc * 16u] >> tshift) & 0xFFFFu;
+      const uint32_t field = WEIGH ? 0u : (stouch[cc * 16u] >> tshift) & 0xFFFFu;
       uint32_t v[LW];
       uint32_t cnt = 0, accbits = 0;
       bool changed = false;
@@ -359,14 +362,14 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
         } else {
           sel = 0x3210u | (((field >> q) & 0x0101u) * 0x44u);
         }
-        uint32_t x = __byte_perm(cur[q], CLK[q], sel);
+        uint32_t x = WEIGH ? cur[q] : __byte_perm(cur[q], CLK[q], sel);
         // checkAT (Alg. 1): two intervals of the cyclic window
         const uint32_t vx = x | G;
         const uint32_t act = (in_range(vx, x, LO1[q], HI1[q]) | in_range(vx, x, LO2[q], HI2[q])) & G;
         cnt += __popc(act);
         accbits |= act >> ((CB == 1 ? 7 : 15) - q);
         // preserveAT for slice t+1 (Alg. 2), only in words holding swept blocks
-        if (swept_mask & (1u << q)) {
+        if (!WEIGH && (swept_mask & (1u << q))) {
           const uint32_t er = (in_range(vx, x, LE1[q], HE1[q]) | in_range(vx, x, LE2[q], HE2[q])) & G;
           const uint32_t m = (er >> (EB - 1)) * EMASK;   // guard bit -> whole-element mask
           x = (x & ~m) | (TWOK & m);
@@ -374,7 +377,7 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
         changed |= (x != cur[q]);
         v[q] = x;
       }
-      if (changed) {   // write back only the lane slices that changed
+      if (!WEIGH && changed) {   // write back only the lane slices that changed
 #pragma unroll
         for (int w4 = 0; w4 < LW / 4; ++w4)
           st_pool(gpool + (size_t)ch * (32u * LW / 4) + w4,
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
       const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, accbits, 1);
       if ((lane & 1u) == 0) {
         gact[(size_t)ch * 16u] = (CB == 1) ? (accbits | (other << 4)) : (accbits | (other << 8));
-        gzero[(size_t)ch * 16u] = 0u;
+        if (!WEIGH) gzero[(size_t)ch * 16u] = 0u;
       }
       // |ATV|^{k'} of every ATV in the chunk with one warp reduction: each ATV's
       // lanes add into their own FIELD-bit slot (max 16*LPA fits the slot)

@@ -1,0 +1,96 @@
+"""SURVEY §8(f) rows built on the same kernels: window queries k' < k, checkpoint /
+restore, and the discrete-window mode with the paper's boundary-spanning example."""
+import numpy as np
+import pytest
+import torch
+
+from gen import PRESETS, Generator
+from oracle import oracle as O
+from paper_1807_01527_b200 import asse
+from parity import compare_pool, compare_reports, to_device
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,N", [("C2", 400_000), ("C3", 1_000_000)])
+def test_query_window_equals_oracle_with_that_kprime(cuda_device, name, N):
+    """asse_query_window(k') after closing slice t == the oracle run with k'."""
+    p = dict(PRESETS[name])
+    k = p["k"]
+    kps = [1, 3, k // 2, k - 1]
+    dev = asse.Asse(**p)
+    oras = {kp: O.Oracle(**dict(p, k_prime=kp)) for kp in kps}
+    g = Generator(name, N=N)
+    for t in range(min(k + 2, 13)):
+        pk = g.slice(t)
+        d, ptr = to_device(pk)
+        dev.scan_slice(ptr, len(pk))
+        dev.end_slice(1)
+        for kp in kps:
+            oras[kp].scan(pk)
+            ro = oras[kp].end_slice(1)
+            rd = dev.query_window(kp, 1)
+            compare_reports(rd, ro, p["theta"], "%s t=%d k'=%d" % (name, t, kp))
+    with pytest.raises(asse.AsseError):
+        dev.query_window(k)
+    # the pool is untouched by queries
+    compare_pool(dev.pool(), oras[kps[-1]].pool(), "pool after queries")
+
+
+def test_checkpoint_roundtrip(cuda_device, tmp_path):
+    p = dict(PRESETS["C1"])
+    a = asse.Asse(**p)
+    g = Generator("C1")
+    for t in range(3):
+        d, ptr = to_device(g.slice(t))
+        a.scan_slice(ptr, g.N)
+        a.end_slice()
+    path = str(tmp_path / "c1.ckpt")
+    a.save_state(path)
+    b = asse.Asse(**p)
+    b.load_state(path)
+    assert b.clock() == a.clock()
+    assert (b.pool() == a.pool()).all()
+    for t in range(3, 6):
+        d, ptr = to_device(g.slice(t))
+        a.scan_slice(ptr, g.N)
+        b.scan_slice(ptr, g.N)
+        ra, rb = a.end_slice(), b.end_slice()
+        assert len(ra) == len(rb) and (ra == rb).all()
+    assert (a.pool() == b.pool()).all()
+    other = asse.Asse(**dict(p, seed=99))
+    with pytest.raises(asse.AsseError):
+        other.load_state(path)
+
+
+def test_boundary_spanner_sliding_vs_discrete(cuda_device):
+    """a host with 512 peers before and 512 after a window boundary is missed
+    by discrete windows and found by the sliding window spanning the boundary
+    (scaled: 200 + 200 peers, theta = 300, g = 512)."""
+    geo = dict(r=4, c=10, u=4, s=6, g=512, theta=300.0, seed=13)
+    H = 0x0A000001
+    rng = np.random.default_rng(4)
+
+    def slice_pk(t):
+        bg = np.stack([rng.integers(0, 2 ** 32, 5000), rng.integers(0, 2 ** 32, 5000)], 1)
+        if t in (1, 2):
+            bips = np.arange(200, dtype=np.uint64) + 1000 * t
+            bg = np.concatenate([bg, np.stack([np.full(200, H), bips], 1)])
+        return np.ascontiguousarray(bg.astype(np.uint32))
+
+    slices = [slice_pk(t) for t in range(4)]
+    # sliding window of k = 2 slices, one slice = one time unit
+    sl = asse.Asse(k=2, **geo)
+    found = []
+    for t, pk in enumerate(slices):
+        d, ptr = to_device(pk)
+        sl.scan_slice(ptr, len(pk))
+        found.append(H in set(sl.end_slice(0)["ip"].tolist()))
+    assert found == [False, False, True, False]
+    # discrete windows of the same length (k = 1, one slice = two time units)
+    ds = asse.Asse(k=1, **geo)
+    for a, b in ((0, 1), (2, 3)):
+        for pk in (slices[a], slices[b]):
+            d, ptr = to_device(pk)
+            ds.scan_slice(ptr, len(pk))
+        assert H not in set(ds.end_slice(0)["ip"].tolist())
