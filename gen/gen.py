@@ -19,6 +19,9 @@ PRESETS = {
     "C3": dict(preset=3, seed=3, N=20_000_000, T=300, k=60, r=4, c=12, u=4, s=6, g=512, theta=1024.0),
     "C4": dict(preset=4, seed=4, N=10_000_000, T=600, k=300, r=4, c=12, u=4, s=6, g=512, theta=1024.0),
     "C5": dict(preset=5, seed=5, N=100_000_000, T=120, k=60, r=4, c=12, u=4, s=6, g=512, theta=1024.0),
+    # the paper's sliding-window geometry (g=4096, r=4, c=14, u=4, k=300)
+    # on the C3 traffic mixture; not a BASELINE.json config
+    "PAPER": dict(preset=3, seed=3, N=20_000_000, T=600, k=300, r=4, c=14, u=4, s=6, g=4096, theta=1024.0),
 }
 
 _lib = None
@@ -110,7 +113,7 @@ class Generator:
 
     def scanners(self):
         L = lib()
-        if self.name not in ("C3", "C4", "C5"):
+        if self.name not in ("C3", "C4", "C5", "PAPER"):
             return []
         return [L.gen_scanner_id(self._h, s) for s in range(50)]
 

@@ -29,7 +29,7 @@ struct Ctx {
   asse_config cfg{};
   // geometry
   uint32_t F = 0, E = 0, W = 0, two_k = 0, kp = 0, a = 0, b = 0, cb = 1, wpa = 0;
-  uint32_t w_theta = 0, lpa_log2 = 0;
+  uint32_t w_theta = 0, lpa_log2 = 0, q_log2 = 0;
   uint32_t shift[kMaxR] = {0};
   uint64_t n_atv = 0, n_at = 0;
   // keys (A14)
@@ -135,7 +135,7 @@ static asse_status validate(const asse_config* cfg, std::string* why) {
   if (p.c + p.u > 24) return bad("device path: c + u <= 24 (32-bit ATV indices)");
   if (p.s < 1 || p.s > p.c) return bad("1 <= s <= c");
   if (!(p.theta > 0)) return bad("theta > 0");
-  if (p.g < 128 || p.g > 512 || (p.g & (p.g - 1))) return bad("device path: g in {128, 256, 512}");
+  if (p.g < 128 || p.g > 4096 || (p.g & (p.g - 1))) return bad("device path: g in {128, 256, ..., 4096}");
   if (p.max_candidates < 1) return bad("max_candidates >= 1");
   if (p.world < 1 || p.world > (uint32_t)kMaxWorld || p.rank >= p.world) return bad("rank < world <= 16");
   const uint32_t W = 32 - p.u;
@@ -178,25 +178,37 @@ static void free_all(Ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
-template <int CB, int LPAL>
+template <int CB, int LPAL, int QL = 0>
 static cudaError_t fold_occ_t(int* occ) {
-  cudaError_t e = cudaFuncSetAttribute(k_fold<CB, LPAL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_fold<CB, LPAL, false, QL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)fold_smem<CB>());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_fold<CB, LPAL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(k_fold<CB, LPAL, true, QL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)fold_smem<CB>());
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_fold<CB, LPAL, false>, kFoldThreads, fold_smem<CB>());
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_fold<CB, LPAL, false, QL>, kFoldThreads,
+                                                       fold_smem<CB>());
 }
-static cudaError_t fold_occupancy(uint32_t cb, uint32_t lpal, int* occ) {
-  if (cb == 1) return lpal == 3 ? fold_occ_t<1, 3>(occ) : lpal == 4 ? fold_occ_t<1, 4>(occ) : fold_occ_t<1, 5>(occ);
-  return lpal == 3 ? fold_occ_t<2, 3>(occ) : lpal == 4 ? fold_occ_t<2, 4>(occ) : fold_occ_t<2, 5>(occ);
+template <int CB>
+static cudaError_t fold_occ_cb(uint32_t lpal, uint32_t ql, int* occ) {
+  if (ql == 1) return fold_occ_t<CB, 5, 1>(occ);
+  if (ql == 2) return fold_occ_t<CB, 5, 2>(occ);
+  if (ql == 3) return fold_occ_t<CB, 5, 3>(occ);
+  return lpal == 3 ? fold_occ_t<CB, 3>(occ) : lpal == 4 ? fold_occ_t<CB, 4>(occ) : fold_occ_t<CB, 5>(occ);
 }
+static cudaError_t fold_occupancy(uint32_t cb, uint32_t lpal, uint32_t ql, int* occ) {
+  return cb == 1 ? fold_occ_cb<1>(lpal, ql, occ) : fold_occ_cb<2>(lpal, ql, occ);
+}
+// fold launch for the geometry: lpal = log2(g/16) capped at 5, ql = log2(g/512) for g > 512
 template <int CB, bool WEIGH = false>
-static void launch_fold(uint32_t lpal, unsigned blocks, cudaStream_t s, const FoldParams& fp) {
-  if (lpal == 3) k_fold<CB, 3, WEIGH><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
-  else if (lpal == 4) k_fold<CB, 4, WEIGH><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
-  else k_fold<CB, 5, WEIGH><<<blocks, kFoldThreads, fold_smem<CB>(), s>>>(fp);
+static void launch_fold(uint32_t lpal, uint32_t ql, unsigned blocks, cudaStream_t s, const FoldParams& fp) {
+  const size_t sm = fold_smem<CB>();
+  if (ql == 1) k_fold<CB, 5, WEIGH, 1><<<blocks, kFoldThreads, sm, s>>>(fp);
+  else if (ql == 2) k_fold<CB, 5, WEIGH, 2><<<blocks, kFoldThreads, sm, s>>>(fp);
+  else if (ql == 3) k_fold<CB, 5, WEIGH, 3><<<blocks, kFoldThreads, sm, s>>>(fp);
+  else if (lpal == 3) k_fold<CB, 3, WEIGH><<<blocks, kFoldThreads, sm, s>>>(fp);
+  else if (lpal == 4) k_fold<CB, 4, WEIGH><<<blocks, kFoldThreads, sm, s>>>(fp);
+  else k_fold<CB, 5, WEIGH><<<blocks, kFoldThreads, sm, s>>>(fp);
 }
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while the
@@ -340,6 +352,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
   c->cb = (c->two_k <= 126) ? 1 : 2;           // A2
   c->wpa = p.g / 32;
   c->lpa_log2 = (p.g == 128) ? 3 : (p.g == 256 ? 4 : 5);
+  c->q_log2 = (p.g <= 512) ? 0 : (p.g == 1024 ? 1 : (p.g == 2048 ? 2 : 3));
   for (uint32_t y = 0; y < p.r; ++y) c->shift[y] = (p.s * y) % c->W;
   c->n_atv = (uint64_t)p.r * c->F * c->E;
   c->n_at = c->n_atv * p.g;
@@ -381,7 +394,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
       CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<2>, kScanThreads, kScanSmem));
     }
     c->scan_grid = std::max(1, occ) * c->sms;
-    CKI(fold_occupancy(c->cb, c->lpa_log2, &occ));
+    CKI(fold_occupancy(c->cb, c->lpa_log2, c->q_log2, &occ));
     c->fold_grid = std::max(1, occ) * c->sms;
   }
   CKI(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
@@ -666,8 +679,8 @@ static asse_status enqueue_end_slice(Ctx* c, uint32_t mode, bool timing, bool ca
   {
     const FoldParams fp = fold_params(c, src, c->kp);
     if (timing) CK(rec(2));
-    if (c->cb == 1) launch_fold<1>(c->lpa_log2, fold_blocks(c), s, fp);
-    else launch_fold<2>(c->lpa_log2, fold_blocks(c), s, fp);
+    if (c->cb == 1) launch_fold<1>(c->lpa_log2, c->q_log2, fold_blocks(c), s, fp);
+    else launch_fold<2>(c->lpa_log2, c->q_log2, fold_blocks(c), s, fp);
     CK(cudaGetLastError());
     if (timing) CK(rec(3));
   }
@@ -818,8 +831,8 @@ asse_status asse_query_window(void* ctx, uint32_t k_prime, asse_report* h_out, u
   CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, s));
   const FoldParams fp = fold_params(c, nullptr, k_prime);
-  if (c->cb == 1) launch_fold<1, true>(c->lpa_log2, fold_blocks(c), s, fp);
-  else launch_fold<2, true>(c->lpa_log2, fold_blocks(c), s, fp);
+  if (c->cb == 1) launch_fold<1, true>(c->lpa_log2, c->q_log2, fold_blocks(c), s, fp);
+  else launch_fold<2, true>(c->lpa_log2, c->q_log2, fold_blocks(c), s, fp);
   CK(cudaGetLastError());
   asse_status st = enqueue_tail(c);
   if (st != ASSE_OK) return st;

@@ -235,7 +235,11 @@ template <int CB> constexpr size_t fold_smem() { return (size_t)kFoldStages * fo
 
 // WEIGH = true: read-only variant for window queries with k' < k on the closed pool
 // (SURVEY §8(f) row 1): no touch fold, no preserveAT, no pool write-back.
-template <int CB, int LPAL, bool WEIGH = false>   // LPAL = log2(lanes per ATV) = log2(g/16): 3, 4 or 5
+// QL = log2(chunks per ATV) for g > 512 (g = 1024..4096, LPAL = 5): with 16 chunks per
+// tile and chunks cc = warp, warp + 8, warp w always sees chunk w mod 2^QL of an ATV, so
+// its per-lane constants stay fixed; the ATV weight is summed across the 2^QL warps
+// with one packed shared-memory atomic (weight << 8 | arrival count).
+template <int CB, int LPAL, bool WEIGH = false, int QL = 0>
 __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
   using S = Swar<CB>;
   constexpr int NW = S::NW, EPW = S::EPW, EB = S::EB;
@@ -282,9 +286,16 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
     }
     return;
   }
-  const uint32_t lia = lane & (LPA - 1u);           // lane within its ATV
+  const uint32_t lia = lane & (LPA - 1u);           // lane within its chunk of the ATV
   const uint32_t two_k = 2u * p.k;
   const uint32_t C0 = *p.C0;
+  const uint32_t qoff = (QL > 0) ? 512u * (warp & ((1u << QL) - 1u)) : 0u;   // chunk offset in the ATV
+  __shared__ uint32_t s_wacc[kFoldStages][kFoldChunksPerTile];
+  if (QL > 0) {
+    for (uint32_t q = threadIdx.x; q < kFoldStages * kFoldChunksPerTile; q += 32 * kFoldConsumerWarps)
+      (&s_wacc[0][0])[q] = 0;
+    asm volatile("bar.sync 1, %0;" :: "r"(32 * kFoldConsumerWarps));   // consumer warps only
+  }
 
   // ---- per-lane, per-element constants (positions i = 16*lia + e), computed once
   uint32_t CLK[NW], LO1[NW], HI1[NW], LO2[NW], HI2[NW], LE1[NW], HE1[NW], LE2[NW], HE2[NW];
@@ -294,7 +305,7 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
     CLK[q] = LO1[q] = HI1[q] = LO2[q] = HI2[q] = LE1[q] = HE1[q] = LE2[q] = HE2[q] = 0;
 #pragma unroll
     for (int e = 0; e < EPW; ++e) {
-      const uint32_t i = 16u * lia + (uint32_t)(q * EPW + e);
+      const uint32_t i = qoff + 16u * lia + (uint32_t)(q * EPW + e);
       uint32_t blk = (p.a > 0) ? min(i / p.a, two_k - 1u) : two_k - 1u;  // A7
       uint32_t clk = (C0 + blk) % two_k;
       uint32_t lo1, hi1 = clk, lo2, hi2;
@@ -397,9 +408,23 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
       if (LPAL == 5) tot = packed;
       else if (LPAL == 4) tot = (packed & 0xFFFFu) + (packed >> 16);
       else tot = (packed & 0xFFu) + ((packed >> 8) & 0xFFu) + ((packed >> 16) & 0xFFu) + (packed >> 24);
-      const uint32_t atv = (ch << (5 - LPAL)) + (lane >> LPAL);
+      const uint32_t atv = (QL > 0) ? (ch >> QL) : (ch << (5 - LPAL)) + (lane >> LPAL);
       const uint32_t yz = atv >> p.c;
-      if (lia == 0 && w >= p.w_theta) {            // super ATV
+      bool is_super;
+      if (QL > 0) {
+        is_super = false;
+        if (lane == 0) {
+          const uint32_t add = (w << 8) | 1u;
+          const uint32_t nv = atomicAdd(&s_wacc[st][cc >> QL], add) + add;
+          if ((nv & 0xFFu) == (1u << QL)) {       // last of the ATV's chunks
+            s_wacc[st][cc >> QL] = 0;             // stage slot reused after the empty barrier
+            is_super = (nv >> 8) >= p.w_theta;
+          }
+        }
+      } else {
+        is_super = (lia == 0 && w >= p.w_theta);
+      }
+      if (is_super) {                              // super ATV
         const uint32_t xcol = atv & (E - 1u);
         const uint32_t slot = atomicAdd(p.sa_cnt + yz, 1u);
         p.sa_list[(size_t)yz * E + slot] = xcol;

@@ -101,6 +101,16 @@ def test_window_variants(cuda_device, k, kp):
         step_both(dev, ora, g.slice(t), geo["theta"], "k=%d k'=%d t=%d" % (k, kp, t))
 
 
+@pytest.mark.parametrize("g,k", [(1024, 10), (2048, 60), (4096, 300), (4096, 4)])
+def test_large_atv(cuda_device, g, k):
+    """g > 512 (the paper's own g = 4096): an ATV spans g/512 fold chunks."""
+    geo = dict(k=k, r=4, c=8, u=4, s=7, g=g, theta=1024.0, seed=31)
+    dev, ora = asse.Asse(**geo), O.Oracle(**geo)
+    gen = Generator("C2", N=300_000)
+    for t in range(5):
+        step_both(dev, ora, gen.slice(t), geo["theta"], "g=%d k=%d t=%d" % (g, k, t))
+
+
 def test_edge_cases_empty_ragged_misaligned_split(cuda_device):
     dev, ora, p = _pair("C1")
     g = Generator("C1")
