@@ -240,7 +240,7 @@ template <int CB> constexpr size_t fold_smem() { return (size_t)kFoldStages * fo
 // its per-lane constants stay fixed; the ATV weight is summed across the 2^QL warps
 // with one packed shared-memory atomic (weight << 8 | arrival count).
 template <int CB, int LPAL, bool WEIGH = false, int QL = 0>
-__global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
+__global__ void __launch_bounds__(kFoldThreads, CB == 1 ? 3 : 2) k_fold(FoldParams p) {
   using S = Swar<CB>;
   constexpr int NW = S::NW, EPW = S::EPW, EB = S::EB;
   constexpr uint32_t G = S::G;
@@ -322,8 +322,10 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
       CLK[q] |= clk << sh;
       LO1[q] |= lo1 << sh; HI1[q] |= (hi1 | gbit) << sh;
       LO2[q] |= lo2 << sh; HI2[q] |= (hi2 | gbit) << sh;
-      LE1[q] |= le1 << sh; HE1[q] |= (he1 | gbit) << sh;
-      LE2[q] |= le2 << sh; HE2[q] |= (he2 | gbit) << sh;
+      if (CB == 1) {
+        LE1[q] |= le1 << sh; HE1[q] |= (he1 | gbit) << sh;
+        LE2[q] |= le2 << sh; HE2[q] |= (he2 | gbit) << sh;
+      }
     }
   }
   swept_mask = __reduce_or_sync(0xFFFFFFFFu, swept_mask);   // warp-uniform per word
@@ -381,7 +383,20 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(FoldParams p) {
         accbits |= act >> ((CB == 1 ? 7 : 15) - q);
         // preserveAT for slice t+1 (Alg. 2), only in words holding swept blocks
         if (!WEIGH && (swept_mask & (1u << q))) {
-          const uint32_t er = (in_range(vx, x, LE1[q], HE1[q]) | in_range(vx, x, LE2[q], HE2[q])) & G;
+          uint32_t er;
+          if (CB == 1) {
+            er = (in_range(vx, x, LE1[q], HE1[q]) | in_range(vx, x, LE2[q], HE2[q])) & G;
+          } else {
+            // u16: sweeps are rare (a = 0 sweeps whole ATVs every k slices), so the Alg. 2
+            // intervals are derived here from the block ACT instead of held in registers:
+            // new ACT 0 (clk = 2k-1) erases [0, k]; new ACT k (clk = k-1) erases [k, 2k-1] and 0
+            const uint32_t ONE = 0x00010001u;
+            const uint32_t d0 = CLK[q] ^ ((two_k - 1u) * ONE), dk = CLK[q] ^ ((p.k - 1u) * ONE);
+            const uint32_t eq0 = ~((d0 | G) - ONE) & G, eqk = ~((dk | G) - ONE) & G;
+            const uint32_t in0k = in_range(vx, x, 0u, (p.k * ONE) | G);
+            const uint32_t inkk = in_range(vx, x, p.k * ONE, ((two_k - 1u) * ONE) | G) | in_range(vx, x, 0u, G);
+            er = ((eq0 & in0k) | (eqk & inkk)) & G;
+          }
           const uint32_t m = (er >> (EB - 1)) * EMASK;   // guard bit -> whole-element mask
           x = (x & ~m) | (TWOK & m);
         }
