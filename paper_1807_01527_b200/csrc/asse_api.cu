@@ -181,13 +181,13 @@ static void free_all(Ctx* c) {
 template <int CB, int LPAL, int QL = 0>
 static cudaError_t fold_occ_t(int* occ) {
   cudaError_t e = cudaFuncSetAttribute(k_fold<CB, LPAL, false, QL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)fold_smem<CB>());
+                                       (int)fold_smem<CB, false>());
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_fold<CB, LPAL, true, QL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)fold_smem<CB>());
+                           (int)fold_smem<CB, true>());
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_fold<CB, LPAL, false, QL>, kFoldThreads,
-                                                       fold_smem<CB>());
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_fold<CB, LPAL, false, QL>, fold_threads<CB, false>(),
+                                                       fold_smem<CB, false>());
 }
 template <int CB>
 static cudaError_t fold_occ_cb(uint32_t lpal, uint32_t ql, int* occ) {
@@ -202,13 +202,14 @@ static cudaError_t fold_occupancy(uint32_t cb, uint32_t lpal, uint32_t ql, int* 
 // fold launch for the geometry: lpal = log2(g/16) capped at 5, ql = log2(g/512) for g > 512
 template <int CB, bool WEIGH = false>
 static void launch_fold(uint32_t lpal, uint32_t ql, unsigned blocks, cudaStream_t s, const FoldParams& fp) {
-  const size_t sm = fold_smem<CB>();
-  if (ql == 1) k_fold<CB, 5, WEIGH, 1><<<blocks, kFoldThreads, sm, s>>>(fp);
-  else if (ql == 2) k_fold<CB, 5, WEIGH, 2><<<blocks, kFoldThreads, sm, s>>>(fp);
-  else if (ql == 3) k_fold<CB, 5, WEIGH, 3><<<blocks, kFoldThreads, sm, s>>>(fp);
-  else if (lpal == 3) k_fold<CB, 3, WEIGH><<<blocks, kFoldThreads, sm, s>>>(fp);
-  else if (lpal == 4) k_fold<CB, 4, WEIGH><<<blocks, kFoldThreads, sm, s>>>(fp);
-  else k_fold<CB, 5, WEIGH><<<blocks, kFoldThreads, sm, s>>>(fp);
+  const size_t sm = fold_smem<CB, WEIGH>();
+  const int th = fold_threads<CB, WEIGH>();
+  if (ql == 1) k_fold<CB, 5, WEIGH, 1><<<blocks, th, sm, s>>>(fp);
+  else if (ql == 2) k_fold<CB, 5, WEIGH, 2><<<blocks, th, sm, s>>>(fp);
+  else if (ql == 3) k_fold<CB, 5, WEIGH, 3><<<blocks, th, sm, s>>>(fp);
+  else if (lpal == 3) k_fold<CB, 3, WEIGH><<<blocks, th, sm, s>>>(fp);
+  else if (lpal == 4) k_fold<CB, 4, WEIGH><<<blocks, th, sm, s>>>(fp);
+  else k_fold<CB, 5, WEIGH><<<blocks, th, sm, s>>>(fp);
 }
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while the

@@ -231,7 +231,18 @@ constexpr uint32_t kFoldChunksPerTile = 16;                    // 16 x 512 ATs p
 constexpr int kFoldStages = 4;
 template <int CB> constexpr uint32_t fold_code_bytes() { return kFoldChunksPerTile * 512u * CB; }
 template <int CB> constexpr uint32_t fold_stage_bytes() { return fold_code_bytes<CB>() + kFoldChunksPerTile * 64u; }
-template <int CB> constexpr size_t fold_smem() { return (size_t)kFoldStages * fold_stage_bytes<CB>(); }
+// u8 full fold: results are staged in shared memory and written back by a storer warp
+// with bulk (TMA) stores: codes, active words and the zeroed touch words of a tile.
+template <int CB, bool WEIGH> constexpr bool fold_tma_out() { return CB == 1 && !WEIGH; }
+constexpr int kFoldOutStages = 2;
+template <int CB, bool WEIGH> constexpr int fold_threads() {
+  return 32 * (kFoldConsumerWarps + 1 + (fold_tma_out<CB, WEIGH>() ? 1 : 0));
+}
+template <int CB> constexpr uint32_t fold_out_stage_bytes() { return fold_code_bytes<CB>() + kFoldChunksPerTile * 64u; }
+template <int CB, bool WEIGH = false> constexpr size_t fold_smem() {
+  return (size_t)kFoldStages * fold_stage_bytes<CB>() +
+         (fold_tma_out<CB, WEIGH>() ? (size_t)kFoldOutStages * fold_out_stage_bytes<CB>() + kFoldChunksPerTile * 64u : 0);
+}
 
 // WEIGH = true: read-only variant for window queries with k' < k on the closed pool
 // (SURVEY §8(f) row 1): no touch fold, no preserveAT, no pool write-back.
@@ -240,7 +251,7 @@ template <int CB> constexpr size_t fold_smem() { return (size_t)kFoldStages * fo
 // its per-lane constants stay fixed; the ATV weight is summed across the 2^QL warps
 // with one packed shared-memory atomic (weight << 8 | arrival count).
 template <int CB, int LPAL, bool WEIGH = false, int QL = 0>
-__global__ void __launch_bounds__(kFoldThreads, CB == 1 ? 3 : 2) k_fold(FoldParams p) {
+__global__ void __launch_bounds__(fold_threads<CB, WEIGH>(), CB == 1 ? 3 : 2) k_fold(FoldParams p) {
   using S = Swar<CB>;
   constexpr int NW = S::NW, EPW = S::EPW, EB = S::EB;
   constexpr uint32_t G = S::G;
@@ -249,8 +260,13 @@ __global__ void __launch_bounds__(kFoldThreads, CB == 1 ? 3 : 2) k_fold(FoldPara
   constexpr uint32_t STAGE_BYTES = fold_stage_bytes<CB>();
   constexpr uint32_t LPA = 1u << LPAL;
   constexpr uint32_t FIELD = 1u << (LPAL);        // bits per packed ATV weight: 8, 16, 32
+  constexpr bool TOUT = fold_tma_out<CB, WEIGH>();
+  constexpr uint32_t OUT_BYTES = fold_out_stage_bytes<CB>();
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kFoldStages], empty[kFoldStages];
+  __shared__ __align__(8) uint64_t out_full[kFoldOutStages], out_empty[kFoldOutStages];
+  uint8_t* const sout = smem + (size_t)kFoldStages * STAGE_BYTES;              // TOUT only
+  uint8_t* const szero = sout + (size_t)kFoldOutStages * OUT_BYTES;            // TOUT only
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   // blocked tile range of this CTA (keeps each warp's (y, z) slab changes rare for AAT)
   const uint32_t n_tiles = (uint32_t)((p.n_chunks + kFoldChunksPerTile - 1) / kFoldChunksPerTile);
@@ -262,10 +278,40 @@ __global__ void __launch_bounds__(kFoldThreads, CB == 1 ? 3 : 2) k_fold(FoldPara
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], kFoldConsumerWarps);
     }
+    if (TOUT)
+      for (int st = 0; st < kFoldOutStages; ++st) {
+        mbar_init(&out_full[st], kFoldConsumerWarps);
+        mbar_init(&out_empty[st], 1);
+      }
     mbar_fence_init();
+  }
+  if (TOUT) {
+    for (uint32_t q = threadIdx.x; q < kFoldChunksPerTile * 16u; q += blockDim.x)
+      reinterpret_cast<uint32_t*>(szero)[q] = 0u;
+    fence_proxy_async_smem();
   }
   __syncthreads();
   if (t0 >= t1) return;
+  if (TOUT && warp == kFoldConsumerWarps + 1) {     // storer warp: TMA bulk write-back
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (uint32_t i = 0; i < t1 - t0; ++i) {
+        const uint32_t os = i % kFoldOutStages;
+        mbar_wait(&out_full[os], (i / kFoldOutStages) & 1u);
+        const uint32_t tile = t0 + i;
+        const uint32_t nch = (uint32_t)umin64(kFoldChunksPerTile, p.n_chunks - (uint64_t)tile * kFoldChunksPerTile);
+        const uint8_t* src = sout + (size_t)os * OUT_BYTES;
+        bulk_s2g(reinterpret_cast<uint8_t*>(p.pool) + (size_t)tile * CODE_BYTES, src, nch * 512u * CB, pol);
+        bulk_s2g(p.active + (size_t)tile * kFoldChunksPerTile * 16u, src + CODE_BYTES, nch * 64u, pol);
+        bulk_s2g(p.touch_zero + (size_t)tile * kFoldChunksPerTile * 16u, szero, nch * 64u, pol);
+        bulk_commit();
+        bulk_wait_read0();                          // out stage may be rewritten
+        mbar_arrive(&out_empty[os]);
+      }
+      bulk_wait0();                                 // writes complete before the kernel ends
+    }
+    return;
+  }
   if (warp == kFoldConsumerWarps) {                 // producer warp: TMA bulk loads
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
@@ -352,6 +398,10 @@ __global__ void __launch_bounds__(kFoldThreads, CB == 1 ? 3 : 2) k_fold(FoldPara
     const uint32_t nch = (uint32_t)umin64(kFoldChunksPerTile, p.n_chunks - (uint64_t)tile * kFoldChunksPerTile);
     const uint8_t* sbase = smem + (size_t)st * STAGE_BYTES;
     const uint4* scodes = reinterpret_cast<const uint4*>(sbase) + lane * (LW / 4);
+    const uint32_t os = i % kFoldOutStages;
+    uint4* ocodes = reinterpret_cast<uint4*>(sout + (size_t)os * OUT_BYTES) + lane * (LW / 4);
+    uint32_t* oact = reinterpret_cast<uint32_t*>(sout + (size_t)os * OUT_BYTES + CODE_BYTES) + (lane >> 1);
+    if (TOUT && i >= kFoldOutStages) mbar_wait(&out_empty[os], ((i / kFoldOutStages) - 1) & 1u);
     const uint32_t* stouch = reinterpret_cast<const uint32_t*>(sbase + CODE_BYTES) + (lane >> 1);
     for (uint32_t cc = warp; cc < nch; cc += kFoldConsumerWarps) {
       const uint32_t ch = tile * kFoldChunksPerTile + cc;
@@ -403,7 +453,11 @@ __global__ void __launch_bounds__(kFoldThreads, CB == 1 ? 3 : 2) k_fold(FoldPara
         changed |= (x != cur[q]);
         v[q] = x;
       }
-      if (!WEIGH && changed) {   // write back only the lane slices that changed
+      if (TOUT) {            // staged for the storer warp's bulk write-back
+#pragma unroll
+        for (int w4 = 0; w4 < LW / 4; ++w4)
+          ocodes[cc * (32u * LW / 4) + w4] = make_uint4(v[4 * w4], v[4 * w4 + 1], v[4 * w4 + 2], v[4 * w4 + 3]);
+      } else if (!WEIGH && changed) {   // write back only the lane slices that changed
 #pragma unroll
         for (int w4 = 0; w4 < LW / 4; ++w4)
           st_pool(gpool + (size_t)ch * (32u * LW / 4) + w4,
@@ -412,8 +466,13 @@ __global__ void __launch_bounds__(kFoldThreads, CB == 1 ? 3 : 2) k_fold(FoldPara
       // active word = even-lane bits | odd-lane bits shifted into the free positions
       const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, accbits, 1);
       if ((lane & 1u) == 0) {
-        gact[(size_t)ch * 16u] = (CB == 1) ? (accbits | (other << 4)) : (accbits | (other << 8));
-        if (!WEIGH) gzero[(size_t)ch * 16u] = 0u;
+        const uint32_t aw = (CB == 1) ? (accbits | (other << 4)) : (accbits | (other << 8));
+        if (TOUT) {
+          oact[cc * 16u] = aw;
+        } else {
+          gact[(size_t)ch * 16u] = aw;
+          if (!WEIGH) gzero[(size_t)ch * 16u] = 0u;
+        }
       }
       // |ATV|^{k'} of every ATV in the chunk with one warp reduction: each ATV's
       // lanes add into their own FIELD-bit slot (max 16*LPA fits the slot)
@@ -454,8 +513,12 @@ __global__ void __launch_bounds__(kFoldThreads, CB == 1 ? 3 : 2) k_fold(FoldPara
       }
       aat_acc += tot;
     }
+    if (TOUT) fence_proxy_async_smem();             // staged writes -> async-proxy reads
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    if (lane == 0) {
+      if (TOUT) mbar_arrive(&out_full[os]);
+      mbar_arrive(&empty[st]);
+    }
   }
   if (lane == 0 && aat_acc) atomicAdd(p.aat + aat_yz, aat_acc);
   nsup = __reduce_add_sync(0xFFFFFFFFu, nsup);
