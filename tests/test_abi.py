@@ -52,7 +52,7 @@ def test_validate_configs(lib):
     base = dict(PRESETS["C3"])
     bad = [
         dict(k=0), dict(k_prime=61), dict(r=1), dict(s=0), dict(s=13), dict(theta=0.0),
-        dict(g=100), dict(g=1024), dict(c=12, s=4, u=4),      # completeness 12+12 < 28
+        dict(g=100), dict(g=8192), dict(g=640), dict(c=12, s=4, u=4),   # completeness 12+12 < 28
         dict(c=7, s=7, r=4, u=4),                              # 7+21 = 28, no duplicate
         dict(world=2, rank=2), dict(max_candidates=0),
     ]
