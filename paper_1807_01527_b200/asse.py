@@ -129,7 +129,6 @@ class Asse:
         self.r, self.c, self.u, self.g = self.cfg.r, self.cfg.c, self.cfg.u, self.cfg.g
         self.F, self.E = 1 << self.u, 1 << self.c
         self._cap = 0
-        self._buf = None
 
     def close(self):
         if getattr(self, "_h", None):
@@ -173,41 +172,33 @@ class Asse:
             ptr, n = pairs.data_ptr(), pairs.numel() // 2
         self._check(self._L.asse_scan_slice_host(self._h, ptr, n))
 
-    def _ensure(self, n):
-        if n > self._cap:
-            self._cap = max(n, 4096)
-            self._buf = np.zeros(self._cap, dtype=REPORT_DTYPE)
+    def _call_reports(self, fn, *args):
+        """Run an entry point that fills a report array; the returned array owns its
+        memory (no copy): sized from the last call's count, retried on CAPACITY."""
+        n = ctypes.c_uint32()
+        cap = max(self._cap, 1024)
+        while True:
+            buf = np.empty(cap, dtype=REPORT_DTYPE)
+            st = fn(self._h, *args[:-1], buf.ctypes.data, cap, ctypes.byref(n), args[-1])
+            if st == E_CAPACITY and n.value > cap:
+                cap = n.value
+                self._cap = cap
+                fn, args = self._L.asse_fetch_reports, (args[-1],)
+                continue
+            self._check(st)
+            self._cap = max(self._cap, n.value)
+            return buf[:n.value]
 
     def end_slice(self, mode=1):
         """Close the slice; returns the reports (numpy REPORT_DTYPE, ascending ip)."""
-        n = ctypes.c_uint32()
-        self._ensure(1)
-        st = self._L.asse_end_slice(self._h, self._buf.ctypes.data, self._cap, ctypes.byref(n), mode)
-        if st == E_CAPACITY:
-            return self.fetch_reports(mode)
-        self._check(st)
-        return self._buf[:n.value].copy()
+        return self._call_reports(self._L.asse_end_slice, mode)
 
     def query_window(self, k_prime, mode=1):
         """Reports of the window of k_prime < k slices ending at the last closed slice."""
-        n = ctypes.c_uint32()
-        self._ensure(1)
-        st = self._L.asse_query_window(self._h, k_prime, self._buf.ctypes.data, self._cap,
-                                       ctypes.byref(n), mode)
-        if st == E_CAPACITY:
-            return self.fetch_reports(mode)
-        self._check(st)
-        return self._buf[:n.value].copy()
+        return self._call_reports(self._L.asse_query_window, k_prime, mode)
 
     def fetch_reports(self, mode=1):
-        n = ctypes.c_uint32()
-        st = self._L.asse_fetch_reports(self._h, None, 0, ctypes.byref(n), mode)
-        if st not in (OK, E_CAPACITY):
-            self._check(st)
-        self._ensure(n.value)
-        self._check(self._L.asse_fetch_reports(self._h, self._buf.ctypes.data, self._cap,
-                                               ctypes.byref(n), mode))
-        return self._buf[:n.value].copy()
+        return self._call_reports(self._L.asse_fetch_reports, mode)
 
     def pool(self):
         n = self._L.asse_pool_size(self._h)
