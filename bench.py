@@ -146,7 +146,8 @@ def workload_config(args, p, n_slice, world, S=None):
            "packets_per_slice": n_slice, "k": p["k"], "theta": p["theta"],
            "sketch": "r=%d x 2^(c+u)=%d x g=%d (c=%d u=%d s=%d)" % (
                p["r"], 1 << (p["c"] + p["u"]), p["g"], p["c"], p["u"], p["s"]),
-           "parallelism": "dp%d" % world,
+           "parallelism": "dp%d" % world + ("" if world == 1 or getattr(args, "replicated", False)
+                                             else " + frame-sharded pool"),
            "l2": "inputs larger than L2 (%d MB per slice per GPU), no flush" % (8 * n_slice // world >> 20)}
     if S is not None:
         cfg["distinct_slices"] = S
@@ -202,6 +203,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=20_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--replicated", action="store_true",
+                    help="N>1: keep the whole pool on every GPU (option R) instead of frame sharding (S)")
     args = ap.parse_args()
 
     p = dict(PRESETS[args.workload])
@@ -233,7 +236,9 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    ctx = asse.Asse(**dict(p, world=world, rank=rank, device=local, max_candidates=1 << 20))
+    shard = 1 if (world > 1 and not args.replicated) else 0
+    ctx = asse.Asse(**dict(p, world=world, rank=rank, device=local, max_candidates=1 << 20,
+                           frame_shard=shard))
     peers = attach_symmetric_peers(ctx) if world > 1 else None
     j0, stride, n_local = shard_slots(n_slice, rank, world)
 

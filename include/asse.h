@@ -46,6 +46,10 @@ typedef struct {
   uint32_t max_candidates; /* CSIP capacity; also sizes the restore join workspace */
   int32_t device;          /* CUDA device ordinal */
   uint32_t world, rank;    /* multi-GPU: packets sharded across `world` ranks */
+  uint32_t frame_shard;    /* 0: every rank keeps the whole pool (replicated, option R);
+                              1: rank d keeps frames [d*F/world, (d+1)*F/world) (option S,
+                              SURVEY §8(e)); world must divide F = 2^u */
+  uint32_t pad;
 } asse_config;
 
 /* One CSIP member (Alg. 4 output) with its Alg. 5 NAT and Eq. 5 estimate. */
@@ -143,7 +147,8 @@ asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint
 
 /* Export the AT pool in the canonical layout [y][z][x][i], one uint16 per AT
  * (values in [0, 2k], 2k = inactive). h_out: caller-owned host array of n entries,
- * n must equal r * 2^u * 2^c * g. Reflects the state after the last end_slice
+ * n must equal asse_pool_size() (r * 2^u * 2^c * g; in option S only this rank's frames,
+ * [y][z - z_first][x][i]). Reflects the state after the last end_slice
  * (post-advance, A32) plus any scans issued since (not yet folded: excluded). */
 asse_status asse_export_pool(void* ctx, uint16_t* h_out, uint64_t n);
 
@@ -157,7 +162,7 @@ asse_status asse_save_state(void* ctx, const char* path);
  * mismatch with ASSE_E_PARAM); pending touches of the context are discarded. */
 asse_status asse_load_state(void* ctx, const char* path);
 
-/* Number of ATs in the pool (r * 2^u * 2^c * g). */
+/* Number of ATs in this context's pool (r * 2^u * 2^c * g, or its frames' share in option S). */
 uint64_t asse_pool_size(const void* ctx);
 
 /* Current slice index t and ACT base C0. */
@@ -176,7 +181,11 @@ void* asse_get_stream(const void* ctx);
  * touch[w]:  device pointers (peer-mapped, e.g. torch symmetric memory) of every
  *            rank's per-slice touch bitmap, each asse_bitmap_bytes() long; touch[rank]
  *            replaces this context's own touch bitmap.
- * merged[w]: same for every rank's merged bitmap.
+ * merged[w]: every rank's merged bitmap, asse_merged_bytes() long (the whole geometry
+ *            in option R, the rank's own frames in option S).
+ * exchange[w]: option S only (else NULL): every rank's report exchange buffer,
+ *            asse_exchange_bytes() long; each rank publishes its frames' reports there
+ *            and gathers every peer's.
  * signal[w]: every rank's signal pad (>= 256 bytes, zero-initialised) used by the
  *            stream-ordered cross-GPU barrier when sync_mode == 0.
  * sync_mode: 0 = device barrier over the signal pads (one process per GPU);
@@ -184,10 +193,21 @@ void* asse_get_stream(const void* ctx);
  *                merges complete before any end_slice; used by single-GPU tests).
  * Buffers are caller-owned and must outlive the context. */
 asse_status asse_attach_peers(void* ctx, void* const* touch, void* const* merged,
-                              void* const* signal, uint32_t sync_mode);
+                              void* const* signal, void* const* exchange, uint32_t sync_mode);
 
-/* Bytes of one touch bitmap (= one merged bitmap): r * 2^u * 2^c * g / 8. */
+/* Bytes of one touch bitmap (whole geometry): r * 2^u * 2^c * g / 8. */
 uint64_t asse_bitmap_bytes(const void* ctx);
+
+/* Bytes of this rank's merged bitmap (its frames only in option S). */
+uint64_t asse_merged_bytes(const void* ctx);
+
+/* Bytes of one report exchange buffer (option S): 64 + max_candidates * sizeof(asse_report). */
+uint64_t asse_exchange_bytes(const void* ctx);
+
+/* Option S with sync_mode 1 (caller-ordered phases on one GPU): after asse_merge on every
+ * rank, fold + restore + NAT of this rank's frames, publishing its reports in its exchange
+ * buffer; then asse_end_slice on every rank gathers all ranks' reports. */
+asse_status asse_end_slice_begin(void* ctx);
 
 /* Multi-GPU phase 1 of end_slice (called by asse_end_slice itself when sync_mode
  * == 0): OR this rank's 1/world shard of every rank's touch bitmap and store the

@@ -25,7 +25,8 @@ SYMBOLS = ["asse_validate", "asse_init", "asse_destroy", "asse_last_error", "ass
            "asse_scan_slice", "asse_scan_slice_host", "asse_end_slice", "asse_fetch_reports",
            "asse_export_pool", "asse_pool_size", "asse_get_clock", "asse_get_keys",
            "asse_get_stats", "asse_get_stream", "asse_attach_peers", "asse_bitmap_bytes",
-           "asse_merge", "asse_query_window", "asse_save_state", "asse_load_state"]
+           "asse_merge", "asse_query_window", "asse_save_state", "asse_load_state",
+           "asse_merged_bytes", "asse_exchange_bytes", "asse_end_slice_begin"]
 
 
 class AsseError(RuntimeError):
@@ -40,7 +41,8 @@ class Config(ctypes.Structure):
                 ("s", ctypes.c_uint32), ("g", ctypes.c_uint32), ("theta", ctypes.c_double),
                 ("seed", ctypes.c_uint64), ("k_prime", ctypes.c_uint32),
                 ("max_candidates", ctypes.c_uint32), ("device", ctypes.c_int32),
-                ("world", ctypes.c_uint32), ("rank", ctypes.c_uint32)]
+                ("world", ctypes.c_uint32), ("rank", ctypes.c_uint32),
+                ("frame_shard", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
 
 
 class Stats(ctypes.Structure):
@@ -88,7 +90,11 @@ def load_library(path=LIB_PATH):
         "asse_get_keys": (i32, [vp, ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u64)]),
         "asse_get_stats": (i32, [vp, ctypes.POINTER(Stats)]),
         "asse_get_stream": (vp, [vp]),
-        "asse_attach_peers": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), u32]),
+        "asse_attach_peers": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                    ctypes.POINTER(vp), u32]),
+        "asse_merged_bytes": (u64, [vp]),
+        "asse_exchange_bytes": (u64, [vp]),
+        "asse_end_slice_begin": (i32, [vp]),
         "asse_bitmap_bytes": (u64, [vp]),
         "asse_merge": (i32, [vp]),
         "asse_query_window": (i32, [vp, u32, vp, u32, ctypes.POINTER(u32), u32]),
@@ -103,9 +109,9 @@ def load_library(path=LIB_PATH):
 
 
 def make_config(k, r, c, u, s, g, theta, seed, k_prime=0, n_slices=0, max_candidates=1 << 20,
-                device=0, world=1, rank=0, **_):
+                device=0, world=1, rank=0, frame_shard=0, **_):
     return Config(k, n_slices, r, c, u, s, g, float(theta), seed, k_prime, max_candidates,
-                  device, world, rank)
+                  device, world, rank, frame_shard, 0)
 
 
 def validate(**kw):
@@ -201,10 +207,11 @@ class Asse:
         return self._call_reports(self._L.asse_fetch_reports, mode)
 
     def pool(self):
+        """Canonical [y][z][x][i] u16 pool (this rank's frames only with frame_shard)."""
         n = self._L.asse_pool_size(self._h)
         out = np.empty(n, dtype=np.uint16)
         self._check(self._L.asse_export_pool(self._h, out.ctypes.data, n))
-        return out.reshape(self.r, self.F, self.E, self.g)
+        return out.reshape(self.r, -1, self.E, self.g)
 
     def save_state(self, path):
         self._check(self._L.asse_save_state(self._h, os.fsencode(path)))
@@ -233,10 +240,20 @@ class Asse:
     def bitmap_bytes(self):
         return self._L.asse_bitmap_bytes(self._h)
 
-    def attach_peers(self, touch, merged, signal=None, sync_mode=0):
+    def merged_bytes(self):
+        return self._L.asse_merged_bytes(self._h)
+
+    def exchange_bytes(self):
+        return self._L.asse_exchange_bytes(self._h)
+
+    def attach_peers(self, touch, merged, signal=None, exchange=None, sync_mode=0):
         w = len(touch)
         arr = lambda xs: (ctypes.c_void_p * w)(*xs) if xs is not None else None
-        self._check(self._L.asse_attach_peers(self._h, arr(touch), arr(merged), arr(signal), sync_mode))
+        self._check(self._L.asse_attach_peers(self._h, arr(touch), arr(merged), arr(signal),
+                                              arr(exchange), sync_mode))
+
+    def end_slice_begin(self):
+        self._check(self._L.asse_end_slice_begin(self._h))
 
     def merge(self):
         self._check(self._L.asse_merge(self._h))

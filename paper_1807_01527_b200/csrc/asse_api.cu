@@ -31,7 +31,10 @@ struct Ctx {
   uint32_t F = 0, E = 0, W = 0, two_k = 0, kp = 0, a = 0, b = 0, cb = 1, wpa = 0;
   uint32_t w_theta = 0, lpa_log2 = 0, q_log2 = 0;
   uint32_t shift[kMaxR] = {0};
-  uint64_t n_atv = 0, n_at = 0;
+  uint64_t n_atv = 0, n_at = 0;       // this context's ATVs / ATs (its frames in option S)
+  uint64_t n_atv_full = 0;            // whole geometry (touch bitmap)
+  uint32_t Fl = 0, z_base = 0;        // local frames and global index of local frame 0
+  bool shard = false;                 // option S (frame-sharded)
   // keys (A14)
   uint32_t A = 0, A_inv = 0;
   uint64_t K_bh = 0;
@@ -93,6 +96,9 @@ struct Ctx {
   uint32_t sync_mode = 0, epoch = 0;
   void* peer_touch[kMaxWorld] = {nullptr};
   void* peer_merged[kMaxWorld] = {nullptr};
+  void* peer_xchg[kMaxWorld] = {nullptr};
+  uint8_t* xchg = nullptr;          // option S: this rank's exchange buffer (count | reports)
+  bool begun = false;               // option S, sync_mode 1: end_slice_begin done
   void* peer_signal[kMaxWorld] = {nullptr};
   asse_stats stats{};
   std::string err;
@@ -138,6 +144,8 @@ static asse_status validate(const asse_config* cfg, std::string* why) {
   if (p.g < 128 || p.g > 4096 || (p.g & (p.g - 1))) return bad("device path: g in {128, 256, ..., 4096}");
   if (p.max_candidates < 1) return bad("max_candidates >= 1");
   if (p.world < 1 || p.world > (uint32_t)kMaxWorld || p.rank >= p.world) return bad("rank < world <= 16");
+  if (p.frame_shard > 1) return bad("frame_shard is 0 or 1");
+  if (p.frame_shard && ((1u << p.u) % p.world)) return bad("frame_shard: world must divide 2^u frames");
   const uint32_t W = 32 - p.u;
   if (p.c + p.s * (p.r - 1) < W) return bad("completeness: c + s(r-1) >= 32-u (P:324, A10)");
   std::vector<int> cover(W, 0);
@@ -286,13 +294,29 @@ static asse_status harvest_scan_timing(Ctx* c) {
 
 static asse_status do_merge(Ctx* c) {
   if (!c->peers) return ASSE_OK;
+  if (c->shard) {
+    MergeShardParams mp{};
+    for (uint32_t w = 0; w < c->cfg.world; ++w) mp.touch[w] = reinterpret_cast<const uint4*>(c->peer_touch[w]);
+    mp.merged = reinterpret_cast<uint4*>(c->merged);
+    mp.world = c->cfg.world;
+    const uint64_t frame4 = (uint64_t)c->E * c->wpa / 4;     // uint4 words per (row, frame) slab
+    mp.row_local = frame4 * c->Fl;
+    mp.row_global = frame4 * c->F;
+    mp.frame_off = frame4 * c->z_base;
+    mp.n = mp.row_local * c->cfg.r;
+    const uint64_t blocks = std::min<uint64_t>((mp.n + 255) / 256, (uint64_t)c->sms * 4);
+    k_merge_shard<<<(unsigned)blocks, 256, 0, c->stream>>>(mp);
+    CK(cudaGetLastError());
+    LAUNCHED(c);
+    return ASSE_OK;
+  }
   MergeParams mp{};
   for (uint32_t w = 0; w < c->cfg.world; ++w) {
     mp.touch[w] = reinterpret_cast<const uint4*>(c->peer_touch[w]);
     mp.merged[w] = reinterpret_cast<uint4*>(c->peer_merged[w]);
   }
   mp.world = c->cfg.world;
-  const uint64_t n4 = c->n_atv * c->wpa / 4;
+  const uint64_t n4 = c->n_atv_full * c->wpa / 4;
   const uint64_t per = (n4 + c->cfg.world - 1) / c->cfg.world;
   mp.lo = per * c->cfg.rank;
   mp.hi = std::min<uint64_t>(n4, mp.lo + per);
@@ -355,7 +379,11 @@ asse_status asse_init(const asse_config* cfg, void** out) {
   c->lpa_log2 = (p.g == 128) ? 3 : (p.g == 256 ? 4 : 5);
   c->q_log2 = (p.g <= 512) ? 0 : (p.g == 1024 ? 1 : (p.g == 2048 ? 2 : 3));
   for (uint32_t y = 0; y < p.r; ++y) c->shift[y] = (p.s * y) % c->W;
-  c->n_atv = (uint64_t)p.r * c->F * c->E;
+  c->shard = p.frame_shard && p.world > 1;
+  c->Fl = c->shard ? c->F / p.world : c->F;
+  c->z_base = c->shard ? p.rank * c->Fl : 0;
+  c->n_atv_full = (uint64_t)p.r * c->F * c->E;
+  c->n_atv = (uint64_t)p.r * c->Fl * c->E;
   c->n_at = c->n_atv * p.g;
   // W_theta = ceil(g - g e^{-theta/g}) (A15)
   double wt = (double)p.g - (double)p.g * exp(-p.theta / (double)p.g);
@@ -399,13 +427,14 @@ asse_status asse_init(const asse_config* cfg, void** out) {
     c->fold_grid = std::max(1, occ) * c->sms;
   }
   CKI(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-  const uint64_t bm_bytes = c->n_atv * c->wpa * 4;
+  const uint64_t bm_bytes = c->n_atv * c->wpa * 4;            // local (active, merged)
+  const uint64_t touch_bytes = c->n_atv_full * c->wpa * 4;     // whole geometry
   CKI(cudaMalloc(&c->pool, c->n_at * c->cb));
-  CKI(cudaMalloc(&c->touch_own, bm_bytes));
+  CKI(cudaMalloc(&c->touch_own, touch_bytes));
   CKI(cudaMalloc(&c->active, bm_bytes));
   {
-    const size_t aat_b = (size_t)p.r * c->F * 8, cnt_b = ((size_t)p.r * c->F * 4 + 255) & ~(size_t)255;
-    const size_t bits_b = (size_t)p.r * c->F * ((c->E + 31) / 32) * 4;
+    const size_t aat_b = (size_t)p.r * c->Fl * 8, cnt_b = ((size_t)p.r * c->Fl * 4 + 255) & ~(size_t)255;
+    const size_t bits_b = (size_t)p.r * c->Fl * ((c->E + 31) / 32) * 4;
     c->scratch_bytes = aat_b + cnt_b + 256 + bits_b;
     CKI(cudaMalloc(&c->scratch, c->scratch_bytes));
     uint8_t* b0 = (uint8_t*)c->scratch;
@@ -414,15 +443,17 @@ asse_status asse_init(const asse_config* cfg, void** out) {
     c->counters = (uint32_t*)(b0 + aat_b + cnt_b);
     c->sa_bits = (uint32_t*)(b0 + aat_b + cnt_b + 256);
   }
-  CKI(cudaMalloc(&c->sa_list, (size_t)p.r * c->F * c->E * 4));
+  CKI(cudaMalloc(&c->sa_list, (size_t)p.r * c->Fl * c->E * 4));
   {
     // restore geometry (Alg. 4 join plan), parts CTAs per frame
     RestoreParams& rp = c->rp0;
     rp.max_cand = p.max_candidates;
-    rp.r = p.r; rp.u = p.u; rp.c = p.c; rp.W = c->W; rp.F = c->F;
+    rp.r = p.r; rp.u = p.u; rp.c = p.c; rp.W = c->W; rp.F = c->Fl;
+    rp.z_base = c->z_base;
+    rp.sys_fence = c->shard ? 1u : 0u;
     rp.A_inv = c->A_inv; rp.g = p.g; rp.wpa = c->wpa; rp.theta = p.theta;
     rp.cells = (double)p.g * (double)c->E;
-    rp.parts = (uint32_t)std::max<int>(1, std::min<int>(16, (2 * c->sms) / (int)c->F));
+    rp.parts = (uint32_t)std::max<int>(1, std::min<int>(16, (2 * c->sms) / (int)c->Fl));
     std::vector<uint8_t> known(c->W, 0);
     for (uint32_t y = 0; y < p.r; ++y) {
       rp.shift[y] = c->shift[y];
@@ -441,7 +472,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
     if (c->restore_smem > 48 * 1024)
       CKI(cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->restore_smem));
     c->ws_cap = 1u << 16;   // partial LBS per CTA and join level
-    CKI(cudaMalloc(&c->ws, (size_t)c->F * rp.parts * 2 * c->ws_cap * 4));
+    CKI(cudaMalloc(&c->ws, (size_t)c->Fl * rp.parts * 2 * c->ws_cap * 4));
   }
   CKI(cudaMalloc(&c->cand, (size_t)p.max_candidates * 4));
   CKI(cudaMalloc(&c->rep, (size_t)p.max_candidates * sizeof(ReportDev)));
@@ -479,7 +510,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
     CKI(cudaGetLastError());
     LAUNCHED(c);
   }
-  CKI(cudaMemsetAsync(c->touch_own, 0, bm_bytes, c->stream));
+  CKI(cudaMemsetAsync(c->touch_own, 0, touch_bytes, c->stream));
   CKI(cudaMemsetAsync(c->active, 0, bm_bytes, c->stream));
   CKI(cudaStreamSynchronize(c->stream));
   c->touch = c->touch_own;
@@ -554,23 +585,30 @@ asse_status asse_scan_slice_host(void* ctx, const uint32_t* h_pairs, uint64_t n_
 }
 
 asse_status asse_attach_peers(void* ctx, void* const* touch, void* const* merged,
-                              void* const* signal, uint32_t sync_mode) {
+                              void* const* signal, void* const* exchange, uint32_t sync_mode) {
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   if (c->cfg.world < 2) { c->err = "attach_peers needs world >= 2"; return ASSE_E_PEER; }
-  if (!touch || !merged || (sync_mode == 0 && !signal)) { c->err = "missing peer arrays"; return ASSE_E_PEER; }
+  if (sync_mode > 1) { c->err = "sync_mode is 0 or 1"; return ASSE_E_PARAM; }
+  if (!touch || !merged || (sync_mode == 0 && !signal) || (c->shard && !exchange)) {
+    c->err = "missing peer arrays"; return ASSE_E_PEER;
+  }
   for (uint32_t w = 0; w < c->cfg.world; ++w) {
-    if (!touch[w] || !merged[w] || (sync_mode == 0 && !signal[w])) { c->err = "null peer pointer"; return ASSE_E_PEER; }
+    if (!touch[w] || !merged[w] || (sync_mode == 0 && !signal[w]) || (c->shard && !exchange[w])) {
+      c->err = "null peer pointer"; return ASSE_E_PEER;
+    }
     c->peer_touch[w] = touch[w];
     c->peer_merged[w] = merged[w];
     c->peer_signal[w] = signal ? signal[w] : nullptr;
+    c->peer_xchg[w] = exchange ? exchange[w] : nullptr;
   }
   CK(cudaSetDevice(c->device));
   CK(cudaStreamSynchronize(c->stream));
-  const uint64_t bm_bytes = c->n_atv * c->wpa * 4;
   c->touch = reinterpret_cast<uint32_t*>(touch[c->cfg.rank]);
   c->merged = reinterpret_cast<uint32_t*>(merged[c->cfg.rank]);
-  CK(cudaMemsetAsync(c->touch, 0, bm_bytes, c->stream));
+  c->xchg = exchange ? reinterpret_cast<uint8_t*>(exchange[c->cfg.rank]) : nullptr;
+  CK(cudaMemsetAsync(c->touch, 0, c->n_atv_full * c->wpa * 4, c->stream));
+  if (c->xchg) CK(cudaMemsetAsync(c->xchg, 0, 64, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   c->sync_mode = sync_mode;
   c->peers = true;
@@ -580,7 +618,18 @@ asse_status asse_attach_peers(void* ctx, void* const* touch, void* const* merged
 uint64_t asse_bitmap_bytes(const void* ctx) {
   if (!ctx) return 0;
   const Ctx* c = static_cast<const Ctx*>(ctx);
+  return c->n_atv_full * c->wpa * 4;
+}
+
+uint64_t asse_merged_bytes(const void* ctx) {
+  if (!ctx) return 0;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
   return c->n_atv * c->wpa * 4;
+}
+
+uint64_t asse_exchange_bytes(const void* ctx) {
+  if (!ctx) return 0;
+  return 64 + (uint64_t)static_cast<const Ctx*>(ctx)->cfg.max_candidates * sizeof(ReportDev);
 }
 
 asse_status asse_merge(void* ctx) {
@@ -614,18 +663,43 @@ static asse_status copy_reports(Ctx* c, asse_report* h_out, uint32_t cap, uint32
 // a7 + a8: restore (Alg. 4, parts CTAs per frame) with NAT and Eq. 5 fused, then the
 // sort by ip; both are launched with programmatic dependent launch so their launch
 // overlaps the previous kernel's tail (griddepcontrol.wait inside).
-static asse_status enqueue_tail(Ctx* c) {
-  const asse_config& p = c->cfg;
+static asse_status enqueue_restore(Ctx* c) {
   cudaStream_t s = c->stream;
   RestoreParams rp = c->rp0;
   rp.sa_cnt = c->sa_cnt; rp.sa_list = c->sa_list; rp.sa_bits = c->sa_bits;
   rp.ws = c->ws; rp.ws_cap = c->ws_cap;
   rp.cand = c->cand; rp.n_cand = c->counters + 0; rp.overflow = c->counters + 1;
   rp.active = c->active; rp.aat = c->aat; rp.reports = c->rep; rp.keys = c->keys; rp.vals = c->vals;
-  CK(launch_pdl(k_restore, dim3(c->F * rp.parts), dim3(512), c->restore_smem, s, rp));
-  CK(launch_pdl(k_sort, dim3(kSortBlocks), dim3(kSortThreads), 0, s, (const ReportDev*)c->rep, c->counters,
-                (uint32_t)p.max_candidates, c->rep_sorted, c->rep_above));
+  if (c->shard) {                   // publish this rank's reports in its exchange buffer
+    rp.n_cand = reinterpret_cast<uint32_t*>(c->xchg);
+    rp.reports = c->xchg + 64;
+  }
+  CK(launch_pdl(k_restore, dim3(c->Fl * rp.parts), dim3(512), c->restore_smem, s, rp));
   return ASSE_OK;
+}
+// option S: clear this rank's whole touch bitmap (every peer has merged from it) and
+// gather every rank's reports
+static asse_status enqueue_gather(Ctx* c) {
+  cudaStream_t s = c->stream;
+  CK(cudaMemsetAsync(c->touch, 0, c->n_atv_full * c->wpa * 4, s));
+  GatherParams gp{};
+  for (uint32_t w = 0; w < c->cfg.world; ++w) gp.xchg[w] = reinterpret_cast<const uint8_t*>(c->peer_xchg[w]);
+  gp.world = c->cfg.world; gp.max_cand = c->cfg.max_candidates;
+  gp.rep = c->rep; gp.keys = c->keys; gp.vals = c->vals; gp.counters = c->counters;
+  k_gather_peers<<<(unsigned)c->sms, 256, 0, s>>>(gp);
+  CK(cudaGetLastError());
+  return ASSE_OK;
+}
+static asse_status enqueue_sort(Ctx* c) {
+  CK(launch_pdl(k_sort, dim3(kSortBlocks), dim3(kSortThreads), 0, c->stream, (const ReportDev*)c->rep,
+                c->counters, (const uint32_t*)(c->counters + (c->shard ? 6 : 0)),
+                (uint32_t)c->cfg.max_candidates, c->rep_sorted, c->rep_above));
+  return ASSE_OK;
+}
+static asse_status enqueue_tail(Ctx* c) {
+  asse_status st = enqueue_restore(c);
+  if (st != ASSE_OK) return st;
+  return enqueue_sort(c);
 }
 
 static FoldParams fold_params(Ctx* c, const uint32_t* src, uint32_t kp) {
@@ -633,7 +707,9 @@ static FoldParams fold_params(Ctx* c, const uint32_t* src, uint32_t kp) {
   FoldParams fp{};
   fp.pool = c->pool;
   fp.touch_src = src;
-  fp.touch_zero = c->touch;
+  // option S: peers still read this rank's whole touch bitmap; it is cleared after the
+  // second barrier (enqueue_gather), so the fold clears its (rewritten) merged input
+  fp.touch_zero = c->shard ? c->merged : c->touch;
   fp.active = c->active;
   fp.aat = c->aat;
   fp.sa_cnt = c->sa_cnt;
@@ -665,30 +741,36 @@ static asse_status enqueue_end_slice(Ctx* c, uint32_t mode, bool timing, bool ca
   if (timing) CK(rec(0));
   // a5: merge (world > 1)
   const uint32_t* src = c->touch;
+  asse_status st;
   if (c->peers) {
     if (c->sync_mode == 0) {
-      asse_status st;
-      if ((st = device_barrier(c)) != ASSE_OK) return st;   // every rank's scans done
+      if ((st = device_barrier(c)) != ASSE_OK) return st;   // every rank's scans (and gathers) done
+      if (c->shard) CK(cudaMemsetAsync(c->xchg, 0, 64, s));   // exchange count of this slice
       if ((st = do_merge(c)) != ASSE_OK) return st;
-      if ((st = device_barrier(c)) != ASSE_OK) return st;   // every shard merged
+      if (!c->shard && (st = device_barrier(c)) != ASSE_OK) return st;   // every shard merged
     }
     src = c->merged;
   }
   if (timing) CK(rec(1));
-  // a6: fold + weights + super + preserve(t+1)
-  CK(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, s));   // AAT, SA counts/bits, counters
-  {
+  if (c->shard && c->sync_mode == 1) {
+    // option S, caller-ordered: fold + restore already ran in asse_end_slice_begin
+    if (!c->begun) { c->err = "frame_shard with sync_mode 1: call asse_end_slice_begin first"; return ASSE_E_STATE; }
+  } else {
+    // a6: fold + weights + super + preserve(t+1)
+    CK(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, s));   // AAT, SA counts/bits, counters
     const FoldParams fp = fold_params(c, src, c->kp);
     if (timing) CK(rec(2));
     if (c->cb == 1) launch_fold<1>(c->lpa_log2, c->q_log2, fold_blocks(c), s, fp);
     else launch_fold<2>(c->lpa_log2, c->q_log2, fold_blocks(c), s, fp);
     CK(cudaGetLastError());
     if (timing) CK(rec(3));
+    if ((st = enqueue_restore(c)) != ASSE_OK) return st;
   }
-  {
-    asse_status st = enqueue_tail(c);
-    if (st != ASSE_OK) return st;
+  if (c->shard) {
+    if (c->sync_mode == 0 && (st = device_barrier(c)) != ASSE_OK) return st;   // all merged + published
+    if ((st = enqueue_gather(c)) != ASSE_OK) return st;
   }
+  if ((st = enqueue_sort(c)) != ASSE_OK) return st;
   if (timing) CK(rec(8));
   return ASSE_OK;
 }
@@ -711,7 +793,7 @@ static asse_status collect(Ctx* c, uint32_t mode, uint32_t K, asse_report* h_out
     c->stats.fold_launches++;
   }
   CK(cudaStreamSynchronize(s));
-  const uint32_t n_cand_raw = c->h_counters[0];
+  const uint32_t n_cand_raw = c->h_counters[c->shard ? 6 : 0];
   const bool overflow = c->h_counters[1] != 0 || n_cand_raw > p.max_candidates;
   const uint32_t n_cand = overflow ? 0 : n_cand_raw;
   bool prefetched = true;
@@ -776,6 +858,30 @@ static asse_status collect(Ctx* c, uint32_t mode, uint32_t K, asse_report* h_out
 
 
 
+asse_status asse_end_slice_begin(void* ctx) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c->shard || !c->peers || c->sync_mode != 1) {
+    c->err = "asse_end_slice_begin is for frame_shard contexts with sync_mode 1";
+    return ASSE_E_STATE;
+  }
+  if (closed_all(c)) { c->err = "all n_slices closed"; return ASSE_E_STATE; }
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  *c->h_clock = c->C0;
+  CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(c->xchg, 0, 64, s));
+  CK(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, s));
+  const FoldParams fp = fold_params(c, c->merged, c->kp);
+  if (c->cb == 1) launch_fold<1>(c->lpa_log2, c->q_log2, fold_blocks(c), s, fp);
+  else launch_fold<2>(c->lpa_log2, c->q_log2, fold_blocks(c), s, fp);
+  CK(cudaGetLastError());
+  asse_status st = enqueue_restore(c);
+  if (st != ASSE_OK) return st;
+  c->begun = true;
+  return ASSE_OK;
+}
+
 asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
@@ -792,8 +898,9 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
   // graph is identical for every slice (host copies stay outside the graph)
   *c->h_clock = c->C0;
   CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
-  if (c->peers && c->sync_mode == 0) {
-    asse_status st = enqueue_end_slice(c, mode, timing, false);   // the barrier epoch changes per slice
+  if ((c->peers && c->sync_mode == 0) || c->shard) {
+    asse_status st = enqueue_end_slice(c, mode, timing, false);   // epochs / phases change per slice
+    c->begun = false;
     if (st != ASSE_OK) return st;
   } else {
     cudaGraphExec_t& ge = c->graph[timing ? 1 : 0][mode];
@@ -824,6 +931,7 @@ asse_status asse_query_window(void* ctx, uint32_t k_prime, asse_report* h_out, u
   if (mode > 1) { c->err = "mode must be 0 or 1"; return ASSE_E_PARAM; }
   if (k_prime < 1 || k_prime >= c->cfg.k) { c->err = "query window needs 1 <= k' < k"; return ASSE_E_PARAM; }
   if (c->t == 0) { c->err = "no closed slice"; return ASSE_E_STATE; }
+  if (c->shard) { c->err = "asse_query_window is not available with frame_shard"; return ASSE_E_STATE; }
   CK(cudaSetDevice(c->device));
   const asse_config& p = c->cfg;
   cudaStream_t s = c->stream;
@@ -851,13 +959,13 @@ asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint
 }
 
 // ------------------------------------------------------------ checkpoint
-// File: "ASSECKPT" | u32 version | u32 code_bytes | u32 k, k', r, c, u, s, g | f64 theta |
+// File: "ASSECKPT" | u32 version (2) | u32 code_bytes | u32 k, k', r, c, u, s, g, world, rank, shard | f64 theta |
 //       u64 seed | u64 t | u32 C0 | u32 pad | pool codes (n_at * code_bytes, canonical values)
 struct CkptHeader {
   char magic[8];
   uint32_t version, code_bytes;
   uint32_t k, kp, r, c, u, s, g;
-  uint32_t pad0;
+  uint32_t world, rank, shard;
   double theta;
   uint64_t seed, t;
   uint32_t C0, pad1;
@@ -869,7 +977,8 @@ asse_status asse_save_state(void* ctx, const char* path) {
   CK(cudaSetDevice(c->device));
   CkptHeader h{};
   memcpy(h.magic, "ASSECKPT", 8);
-  h.version = 1; h.code_bytes = c->cb;
+  h.version = 2; h.code_bytes = c->cb;
+  h.world = c->cfg.world; h.rank = c->cfg.rank; h.shard = c->shard ? 1 : 0;
   h.k = c->cfg.k; h.kp = c->kp; h.r = c->cfg.r; h.c = c->cfg.c; h.u = c->cfg.u; h.s = c->cfg.s;
   h.g = c->cfg.g; h.theta = c->cfg.theta; h.seed = c->cfg.seed; h.t = c->t; h.C0 = c->C0;
   std::vector<uint8_t> buf(c->n_at * c->cb);
@@ -892,7 +1001,11 @@ asse_status asse_load_state(void* ctx, const char* path) {
   CkptHeader h{};
   std::vector<uint8_t> buf(c->n_at * c->cb);
   bool ok = fread(&h, sizeof(h), 1, f) == 1;
-  if (ok && (memcmp(h.magic, "ASSECKPT", 8) != 0 || h.version != 1)) { fclose(f); c->err = "not an ASSE checkpoint (v1)"; return ASSE_E_PARAM; }
+  if (ok && (memcmp(h.magic, "ASSECKPT", 8) != 0 || h.version != 2)) { fclose(f); c->err = "not an ASSE checkpoint (v2)"; return ASSE_E_PARAM; }
+  if (ok && h.shard != (c->shard ? 1u : 0u)) { fclose(f); c->err = "checkpoint frame sharding differs"; return ASSE_E_PARAM; }
+  if (ok && h.shard && (h.world != c->cfg.world || h.rank != c->cfg.rank)) {
+    fclose(f); c->err = "frame-sharded checkpoint of another rank/world"; return ASSE_E_PARAM;
+  }
   if (ok && (h.code_bytes != c->cb || h.k != c->cfg.k || h.kp != c->kp || h.r != c->cfg.r || h.c != c->cfg.c ||
              h.u != c->cfg.u || h.s != c->cfg.s || h.g != c->cfg.g || h.theta != c->cfg.theta ||
              h.seed != c->cfg.seed)) {
@@ -905,7 +1018,7 @@ asse_status asse_load_state(void* ctx, const char* path) {
   if (!ok) { c->err = std::string("short read from ") + path; return ASSE_E_PARAM; }
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaMemcpy(c->pool, buf.data(), buf.size(), cudaMemcpyHostToDevice));
-  CK(cudaMemset(c->touch, 0, c->n_atv * c->wpa * 4));
+  CK(cudaMemset(c->touch, 0, c->n_atv_full * c->wpa * 4));
   c->t = h.t;
   c->C0 = h.C0;
   c->have_reports = false;

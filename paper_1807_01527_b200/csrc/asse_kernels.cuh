@@ -551,6 +551,8 @@ struct RestoreParams {
   uint32_t* keys;                // ip per slot (device-wide sort)
   uint32_t* vals;                // slot index (device-wide sort)
   uint32_t A_inv, g, wpa;
+  uint32_t z_base;               // global index of local frame 0 (option S: rank * F_local)
+  uint32_t sys_fence;            // option S: publish the reports to peers (system-scope fence)
   double theta, cells;           // cells = g * 2^c
 };
 
@@ -661,7 +663,7 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
       }
       if (slot >= p.max_cand) { *p.overflow = 1u; continue; }
       // a restored candidate: f(ip) = (LBS << u) | z, ip = A^{-1} f
-      const uint32_t h = (p.u ? (nl << p.u) : nl) | z;
+      const uint32_t h = (p.u ? (nl << p.u) : nl) | (p.z_base + z);
       p.cand[slot] = h;
       // Alg. 5 NAT: ATs active in all r ATVs of the candidate
       const uint64_t DL = (uint64_t)nl | ((uint64_t)nl << p.W);
@@ -700,6 +702,7 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
     if (threadIdx.x == 0) s_nin = (uint32_t)min((uint64_t)s_next, (uint64_t)kPartSmem + p.ws_cap);
     __syncthreads();
   }
+  if (p.sys_fence) __threadfence_system();
   pdl_trigger();
 }
 
@@ -769,7 +772,8 @@ __device__ __forceinline__ void block_sort_emit(const ReportDev* __restrict__ re
 }
 
 __global__ void __launch_bounds__(kSortThreads) k_sort(const ReportDev* __restrict__ rep, uint32_t* counters,
-                                                       uint32_t max_cand, ReportDev* __restrict__ sorted,
+                                                       const uint32_t* n_ptr, uint32_t max_cand,
+                                                       ReportDev* __restrict__ sorted,
                                                        ReportDev* __restrict__ above) {
   using S16 = cub::BlockRadixSort<uint32_t, kSortThreads, 16, uint32_t, 4>;
   union Smem {
@@ -779,7 +783,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort(const ReportDev* __restri
   __shared__ __align__(16) Smem sm;
   __shared__ uint32_t warp_cnt[kSortThreads / 32];
   pdl_wait();                                          // k_restore's reports and |CSIP|
-  const uint32_t n = min(counters[0], max_cand);
+  const uint32_t n = min(*n_ptr, max_cand);
   if (n == 0) return;
   if (n > kSortCap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) counters[5] = 1u;
@@ -868,6 +872,70 @@ __global__ void __launch_bounds__(256) k_merge_or(MergeParams p) {
   // make this thread's peer stores visible system-wide before the kernel completes;
   // the following k_barrier release/acquire then orders them before every rank's fold
   __threadfence_system();
+}
+
+// a5, option S: rank d ORs every rank's touch words of its own frames into its local
+// merged bitmap (a reduce-scatter over NVLink; frames of a row are contiguous).
+struct MergeShardParams {
+  const uint4* touch[kMaxWorld];   // every rank's (whole-geometry) touch bitmap
+  uint4* merged;                   // this rank's merged bitmap (own frames only)
+  uint32_t world;
+  uint64_t row_local, row_global;  // uint4 words per row: own frames / all frames
+  uint64_t frame_off;              // uint4 offset of the first own frame inside a row
+  uint64_t n;                      // uint4 words of the local merged bitmap
+};
+__global__ void __launch_bounds__(256) k_merge_shard(MergeShardParams p) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < p.n;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t y = q / p.row_local, rest = q % p.row_local;
+    const uint64_t gq = y * p.row_global + p.frame_off + rest;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (uint32_t w = 0; w < p.world; ++w) {
+      const uint4 v = __ldcv(p.touch[w] + gq);
+      acc.x |= v.x; acc.y |= v.y; acc.z |= v.z; acc.w |= v.w;
+    }
+    p.merged[q] = acc;
+  }
+}
+
+// Option S: gather every rank's published reports (count at byte 0, reports at byte
+// 64 of its exchange buffer) into this rank's report array, with keys/values for the
+// device-wide sort; counters[6] = total, counters[1] = overflow.
+struct GatherParams {
+  const uint8_t* xchg[kMaxWorld];
+  uint32_t world, max_cand;
+  ReportDev* rep;
+  uint32_t* keys;
+  uint32_t* vals;
+  uint32_t* counters;
+};
+__global__ void __launch_bounds__(256) k_gather_peers(GatherParams p) {
+  __shared__ uint32_t s_off[kMaxWorld + 1];
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (uint32_t w = 0; w < p.world; ++w) {
+      s_off[w] = acc;
+      acc += __ldcv(reinterpret_cast<const uint32_t*>(p.xchg[w]));
+    }
+    s_off[p.world] = acc;
+    if (blockIdx.x == 0) {
+      p.counters[6] = acc;
+      if (acc > p.max_cand) p.counters[1] = 1u;
+    }
+  }
+  __syncthreads();
+  const uint32_t total = min(s_off[p.world], p.max_cand);
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
+    uint32_t w = 0;
+    while (q >= s_off[w + 1]) ++w;
+    const ReportDev* src = reinterpret_cast<const ReportDev*>(p.xchg[w] + 64) + (q - s_off[w]);
+    ReportDev r;
+    r.ip = __ldcv(&src->ip); r.nat = __ldcv(&src->nat);
+    r.estimate = __ldcv(&src->estimate); r.flags = __ldcv(&src->flags); r.pad = 0;
+    p.rep[q] = r;
+    p.keys[q] = r.ip;
+    p.vals[q] = q;
+  }
 }
 
 struct BarrierParams {

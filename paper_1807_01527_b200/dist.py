@@ -28,9 +28,10 @@ def attach_symmetric_peers(ctx, group=None):
 
     group = group or dist.group.WORLD
     dev = torch.device("cuda", torch.cuda.current_device())
-    nbytes = ctx.bitmap_bytes()
+    shard = bool(ctx.cfg.frame_shard)
+    sizes = [ctx.bitmap_bytes(), ctx.merged_bytes(), 256] + ([ctx.exchange_bytes()] if shard else [])
     bufs, ptrs = [], []
-    for size in (nbytes, nbytes, 256):
+    for size in sizes:
         t = symm_mem.empty(size, dtype=torch.uint8, device=dev)
         t.zero_()
         h = symm_mem.rendezvous(t, group)
@@ -38,21 +39,24 @@ def attach_symmetric_peers(ctx, group=None):
         ptrs.append(list(h.buffer_ptrs))
     torch.cuda.synchronize()
     dist.barrier(group)
-    ctx.attach_peers(ptrs[0], ptrs[1], ptrs[2], sync_mode=0)
+    ctx.attach_peers(ptrs[0], ptrs[1], ptrs[2], ptrs[3] if shard else None, sync_mode=0)
     return bufs
 
 
 def attach_local_peers(ctxs):
     """Single-GPU 'virtual ranks' (tests): every context gets plain device buffers
     and the caller orders the phases (sync_mode 1): scan all ranks, then
-    ctx.merge() for every rank, synchronize, then end_slice for every rank."""
+    ctx.merge() for every rank, synchronize, (frame_shard: end_slice_begin for every
+    rank, synchronize,) then end_slice for every rank."""
     import torch
-    nbytes = ctxs[0].bitmap_bytes()
-    touch = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in ctxs]
-    merged = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in ctxs]
+    shard = bool(ctxs[0].cfg.frame_shard)
+    touch = [torch.zeros(c.bitmap_bytes(), dtype=torch.uint8, device="cuda") for c in ctxs]
+    merged = [torch.zeros(c.merged_bytes(), dtype=torch.uint8, device="cuda") for c in ctxs]
+    xchg = [torch.zeros(c.exchange_bytes(), dtype=torch.uint8, device="cuda") for c in ctxs] if shard else []
     tp = [t.data_ptr() for t in touch]
     mp = [t.data_ptr() for t in merged]
+    xp = [t.data_ptr() for t in xchg] if shard else None
     torch.cuda.synchronize()
     for c in ctxs:
-        c.attach_peers(tp, mp, None, sync_mode=1)
-    return touch, merged
+        c.attach_peers(tp, mp, None, xp, sync_mode=1)
+    return touch, merged, xchg

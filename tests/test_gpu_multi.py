@@ -17,11 +17,14 @@ from parity import compare_pool, compare_reports, to_device
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("shard", [0, 1])
 @pytest.mark.parametrize("name,D,N,T", [("C1", 2, None, 5), ("C2", 4, 600_000, 4),
-                                        ("C3", 8, 2_000_000, 3)])
-def test_virtual_ranks_merge_equals_single(cuda_device, name, D, N, T):
+                                        ("C3", 8, 2_000_000, 3), ("C4", 16, 400_000, 3)])
+def test_virtual_ranks_merge_equals_single(cuda_device, name, D, N, T, shard):
+    """shard 0: replicated pools (option R); shard 1: rank d keeps frames
+    [d F/D, (d+1) F/D) (option S) and the reports are gathered from every rank."""
     p = dict(PRESETS[name])
-    ranks = [asse.Asse(**dict(p, world=D, rank=d)) for d in range(D)]
+    ranks = [asse.Asse(**dict(p, world=D, rank=d, frame_shard=shard)) for d in range(D)]
     bufs = attach_local_peers(ranks)
     single = asse.Asse(**p)
     ora = O.Oracle(**p)
@@ -38,6 +41,10 @@ def test_virtual_ranks_merge_equals_single(cuda_device, name, D, N, T):
         for ctx in ranks:
             ctx.merge()
         torch.cuda.synchronize()
+        if shard:
+            for ctx in ranks:
+                ctx.end_slice_begin()
+            torch.cuda.synchronize()
         reps = [ctx.end_slice(1) for ctx in ranks]
         dfull, ptr = to_device(pk)
         single.scan_slice(ptr, len(pk))
@@ -45,10 +52,13 @@ def test_virtual_ranks_merge_equals_single(cuda_device, name, D, N, T):
         ora.scan(pk)
         ro = ora.end_slice(1)
         compare_reports(rs, ro, p["theta"], "%s single t=%d" % (name, t))
-        pool0 = ranks[0].pool()
+        if shard:   # the rank pools are the frame slices of the whole pool
+            pool0 = np.concatenate([ctx.pool() for ctx in ranks], axis=1)
+        else:
+            pool0 = ranks[0].pool()
         compare_pool(pool0, ora.pool(), "%s merged t=%d" % (name, t))
         for d in range(D):
             compare_reports(reps[d], ro, p["theta"], "%s rank %d t=%d" % (name, d, t))
-            if d:
+            if d and not shard:
                 assert (ranks[d].pool() == pool0).all()
     del bufs
