@@ -49,7 +49,9 @@ typedef struct {
   uint32_t frame_shard;    /* 0: every rank keeps the whole pool (replicated, option R);
                               1: rank d keeps frames [d*F/world, (d+1)*F/world) (option S,
                               SURVEY §8(e)); world must divide F = 2^u */
-  uint32_t pad;
+  uint32_t mangle;         /* 0: f(aip) = A*aip mod 2^32, A odd (A8);
+                              1: f(aip) = A*aip mod p, p = 2^32+15 prime, cycle-walked into
+                              32 bits (P:305 literal) */
 } asse_config;
 
 /* One CSIP member (Alg. 4 output) with its Alg. 5 NAT and Eq. 5 estimate. */
@@ -168,8 +170,8 @@ uint64_t asse_pool_size(const void* ctx);
 /* Current slice index t and ACT base C0. */
 asse_status asse_get_clock(const void* ctx, uint64_t* t, uint32_t* C0);
 
-/* Keys derived from the seed (A14): A, A^{-1} mod 2^32, K_bh. For tests. */
-asse_status asse_get_keys(const void* ctx, uint32_t* A, uint32_t* A_inv, uint64_t* K_bh);
+/* Keys derived from the seed (A14): A, A^{-1} (mod 2^32, or mod p with mangle = 1), K_bh. */
+asse_status asse_get_keys(const void* ctx, uint64_t* A, uint64_t* A_inv, uint64_t* K_bh);
 
 /* Statistics; out: caller-owned asse_stats. */
 asse_status asse_get_stats(const void* ctx, asse_stats* out);

@@ -40,6 +40,8 @@ typedef struct {
   double theta;
   uint64_t seed;
   uint32_t max_candidates;
+  uint32_t mangle;       /* 0: f(x) = A x mod 2^32, A odd (A8); 1: f(x) = A x mod p,
+                            p = 2^32 + 15 prime, cycle-walked into 32 bits (P:305 literal) */
 } oracle_params;
 
 typedef struct {
@@ -54,7 +56,7 @@ typedef struct {
   uint32_t a, b;          /* ATV block sizes */
   uint32_t C0;            /* ACT of block 0 */
   uint64_t t;             /* current slice */
-  uint32_t A, A_inv;      /* mangling key and inverse (A8) */
+  uint64_t A, A_inv;      /* mangling key and inverse (A8 or mod p) */
   uint64_t K_bh;          /* BH key (A13) */
   uint16_t* pool;         /* AT[y][z][x][i] */
   /* per-slice end results */
@@ -151,9 +153,28 @@ uint32_t oracle_act(const oracle_t* o, uint32_t i) {
 
 /* ------------------------------------------------------------------ RRH */
 
-/* f(aip) = A * aip mod 2^32 (A8) */
-uint32_t oracle_mangle(const oracle_t* o, uint32_t ip) { return (uint32_t)(o->A * ip); }
-uint32_t oracle_unmangle(const oracle_t* o, uint32_t h) { return (uint32_t)(o->A_inv * h); }
+#define MANGLE_P 4294967311ULL   /* the smallest prime above 2^32 */
+
+static uint64_t mulmod_p(uint64_t a, uint64_t b) {
+  return (uint64_t)(((unsigned __int128)a * b) % MANGLE_P);
+}
+/* f(aip) = A * aip mod 2^32 (A8), or — SURVEY §8(f) row 4, the paper-literal form —
+ * f(aip) = A * aip mod p with p prime > 2^32. The latter is a bijection of
+ * [0, p); the values >= 2^32 it yields for 32-bit inputs are stepped through f again
+ * (cycle walking) until they fit in 32 bits, which keeps f a bijection of [0, 2^32). */
+uint32_t oracle_mangle(const oracle_t* o, uint32_t ip) {
+  if (!o->p.mangle) return (uint32_t)(o->A * ip);
+  uint64_t y = mulmod_p(o->A, ip);
+  while (y >= 4294967296ULL) y = mulmod_p(o->A, y);
+  return (uint32_t)y;
+}
+/* f^{-1}(h) = A^{-1} h ("aip could be regain by f^{-1}"), walked the same way. */
+uint32_t oracle_unmangle(const oracle_t* o, uint32_t h) {
+  if (!o->p.mangle) return (uint32_t)(o->A_inv * h);
+  uint64_t x = mulmod_p(o->A_inv, h);
+  while (x >= 4294967296ULL) x = mulmod_p(o->A_inv, x);
+  return (uint32_t)x;
+}
 
 /* Z(aip) = RBS(f(aip), u); LBS = the left 32-u bits, LBS[p] its p-th bit
  * counted from the least significant end (A9); x_y[j] = LBS[(s*y + j) mod (32-u)]
@@ -230,6 +251,7 @@ int oracle_validate(const oracle_params* p, char* why, size_t n) {
   if (p->u > 31 || p->c < 1 || p->c + p->u > 32) BAD("c >= 1, u <= 31, c + u <= 32");
   if (p->s < 1 || p->s > p->c) BAD("1 <= s <= c");
   if (!(p->theta > 0)) BAD("theta > 0");
+  if (p->mangle > 1) BAD("mangle is 0 or 1");
   uint32_t W = 32 - p->u;
   if (p->c + p->s * (p->r - 1) < W) BAD("completeness: c + s(r-1) >= 32-u");
   uint32_t cover[32] = {0};
@@ -254,9 +276,18 @@ oracle_t* oracle_new(const oracle_params* p, char* why, size_t n) {
   o->a = p->g / (2 * p->k);
   o->b = p->g - o->a * (2 * p->k - 1);
   uint64_t st = p->seed;
-  o->A = (uint32_t)(sm64_next(&st) >> 32) | 1u;
-  o->K_bh = sm64_next(&st);
-  o->A_inv = inverse_mod_2_32(o->A);
+  if (!p->mangle) {
+    o->A = (uint32_t)(sm64_next(&st) >> 32) | 1u;
+    o->K_bh = sm64_next(&st);
+    o->A_inv = inverse_mod_2_32((uint32_t)o->A);
+  } else {
+    /* A uniform in [1, p-1]; A^{-1} = A^{p-2} mod p (Fermat) */
+    o->A = sm64_next(&st) % (MANGLE_P - 1) + 1;
+    o->K_bh = sm64_next(&st);
+    uint64_t r = 1, b = o->A, e = MANGLE_P - 2;
+    while (e) { if (e & 1) r = mulmod_p(r, b); b = mulmod_p(b, b); e >>= 1; }
+    o->A_inv = r;
+  }
   size_t n_atv = (size_t)p->r * o->F * o->E;
   size_t n_at = n_atv * p->g;
   o->pool = (uint16_t*)malloc(n_at * sizeof(uint16_t));
@@ -281,7 +312,7 @@ void oracle_free(oracle_t* o) {
   free(o);
 }
 
-void oracle_keys(const oracle_t* o, uint32_t* A, uint32_t* A_inv, uint64_t* K_bh) {
+void oracle_keys(const oracle_t* o, uint64_t* A, uint64_t* A_inv, uint64_t* K_bh) {
   *A = o->A; *A_inv = o->A_inv; *K_bh = o->K_bh;
 }
 void oracle_blocks(const oracle_t* o, uint32_t* a, uint32_t* b) { *a = o->a; *b = o->b; }

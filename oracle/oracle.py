@@ -21,7 +21,7 @@ class _Params(ctypes.Structure):
     _fields_ = [("k", ctypes.c_uint32), ("k_prime", ctypes.c_uint32), ("r", ctypes.c_uint32),
                 ("c", ctypes.c_uint32), ("u", ctypes.c_uint32), ("s", ctypes.c_uint32),
                 ("g", ctypes.c_uint32), ("theta", ctypes.c_double), ("seed", ctypes.c_uint64),
-                ("max_candidates", ctypes.c_uint32)]
+                ("max_candidates", ctypes.c_uint32), ("mangle", ctypes.c_uint32)]
 
 
 _lib = None
@@ -108,8 +108,8 @@ def w_theta(g, theta):
     return lib().oracle_w_theta(g, theta)
 
 
-def _params(k, r, c, u, s, g, theta, seed, k_prime=0, max_candidates=1 << 24, **_):
-    return _Params(k, k_prime or k, r, c, u, s, g, float(theta), seed, max_candidates)
+def _params(k, r, c, u, s, g, theta, seed, k_prime=0, max_candidates=1 << 24, mangle=0, **_):
+    return _Params(k, k_prime or k, r, c, u, s, g, float(theta), seed, max_candidates, mangle)
 
 
 def validate(**kw):
@@ -140,7 +140,7 @@ class Oracle:
 
     # ---- keys / hashing
     def keys(self):
-        A, Ai, K = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint64()
+        A, Ai, K = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         lib().oracle_keys(self._h, ctypes.byref(A), ctypes.byref(Ai), ctypes.byref(K))
         return A.value, Ai.value, K.value
 

@@ -42,7 +42,7 @@ class Config(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("k_prime", ctypes.c_uint32),
                 ("max_candidates", ctypes.c_uint32), ("device", ctypes.c_int32),
                 ("world", ctypes.c_uint32), ("rank", ctypes.c_uint32),
-                ("frame_shard", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
+                ("frame_shard", ctypes.c_uint32), ("mangle", ctypes.c_uint32)]
 
 
 class Stats(ctypes.Structure):
@@ -87,7 +87,7 @@ def load_library(path=LIB_PATH):
         "asse_export_pool": (i32, [vp, vp, u64]),
         "asse_pool_size": (u64, [vp]),
         "asse_get_clock": (i32, [vp, ctypes.POINTER(u64), ctypes.POINTER(u32)]),
-        "asse_get_keys": (i32, [vp, ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u64)]),
+        "asse_get_keys": (i32, [vp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]),
         "asse_get_stats": (i32, [vp, ctypes.POINTER(Stats)]),
         "asse_get_stream": (vp, [vp]),
         "asse_attach_peers": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
@@ -109,9 +109,9 @@ def load_library(path=LIB_PATH):
 
 
 def make_config(k, r, c, u, s, g, theta, seed, k_prime=0, n_slices=0, max_candidates=1 << 20,
-                device=0, world=1, rank=0, frame_shard=0, **_):
+                device=0, world=1, rank=0, frame_shard=0, mangle=0, **_):
     return Config(k, n_slices, r, c, u, s, g, float(theta), seed, k_prime, max_candidates,
-                  device, world, rank, frame_shard, 0)
+                  device, world, rank, frame_shard, mangle)
 
 
 def validate(**kw):
@@ -225,7 +225,7 @@ class Asse:
         return t.value, c0.value
 
     def keys(self):
-        A, Ai, K = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint64()
+        A, Ai, K = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         self._check(self._L.asse_get_keys(self._h, ctypes.byref(A), ctypes.byref(Ai), ctypes.byref(K)))
         return A.value, Ai.value, K.value
 

@@ -36,7 +36,7 @@ struct Ctx {
   uint32_t Fl = 0, z_base = 0;        // local frames and global index of local frame 0
   bool shard = false;                 // option S (frame-sharded)
   // keys (A14)
-  uint32_t A = 0, A_inv = 0;
+  uint64_t A = 0, A_inv = 0;
   uint64_t K_bh = 0;
   // clock (A3)
   uint32_t C0 = 0;
@@ -145,6 +145,7 @@ static asse_status validate(const asse_config* cfg, std::string* why) {
   if (p.max_candidates < 1) return bad("max_candidates >= 1");
   if (p.world < 1 || p.world > (uint32_t)kMaxWorld || p.rank >= p.world) return bad("rank < world <= 16");
   if (p.frame_shard > 1) return bad("frame_shard is 0 or 1");
+  if (p.mangle > 1) return bad("mangle is 0 or 1");
   if (p.frame_shard && ((1u << p.u) % p.world)) return bad("frame_shard: world must divide 2^u frames");
   const uint32_t W = 32 - p.u;
   if (p.c + p.s * (p.r - 1) < W) return bad("completeness: c + s(r-1) >= 32-u (P:324, A10)");
@@ -264,10 +265,14 @@ static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cuda
     e1 = c->ev_free.back(); c->ev_free.pop_back();
     CK(cudaEventRecord(e0, st));
   }
-  if (c->cb == 1)
-    k_scan<1><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(reinterpret_cast<const uint2*>(d_pairs), n, p);
-  else
-    k_scan<2><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(reinterpret_cast<const uint2*>(d_pairs), n, p);
+  const uint2* pk = reinterpret_cast<const uint2*>(d_pairs);
+  if (c->cfg.mangle) {
+    if (c->cb == 1) k_scan<1, true><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
+    else k_scan<2, true><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
+  } else {
+    if (c->cb == 1) k_scan<1><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
+    else k_scan<2><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
+  }
   CK(cudaGetLastError());
   LAUNCHED(c);
   c->stats.scan_launches++;
@@ -390,9 +395,20 @@ asse_status asse_init(const asse_config* cfg, void** out) {
   double wc = ceil(wt);
   c->w_theta = (wc > (double)p.g) ? p.g + 1 : (uint32_t)wc;
   uint64_t st = p.seed;
-  c->A = (uint32_t)(splitmix_next(&st) >> 32) | 1u;
-  c->K_bh = splitmix_next(&st);
-  c->A_inv = inv_newton(c->A);
+  if (!p.mangle) {
+    c->A = (uint32_t)(splitmix_next(&st) >> 32) | 1u;
+    c->K_bh = splitmix_next(&st);
+    c->A_inv = inv_newton((uint32_t)c->A);
+  } else {                                    // A in [1, p-1]; A^{-1} = A^{p-2} (Fermat)
+    c->A = splitmix_next(&st) % (kMangleP - 1) + 1;
+    c->K_bh = splitmix_next(&st);
+    uint64_t r = 1, b = c->A;
+    for (uint64_t e = kMangleP - 2; e; e >>= 1) {
+      if (e & 1) r = mulmod_p(r, b);
+      b = mulmod_p(b, b);
+    }
+    c->A_inv = r;
+  }
   c->device = p.device;
   c->stats.w_theta = c->w_theta;
   c->stats.code_bytes = c->cb;
@@ -415,13 +431,12 @@ asse_status asse_init(const asse_config* cfg, void** out) {
   CKI(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   {
     int occ = 0;
-    if (c->cb == 1) {
-      CKI(cudaFuncSetAttribute(k_scan<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem));
-      CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<1>, kScanThreads, kScanSmem));
-    } else {
-      CKI(cudaFuncSetAttribute(k_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem));
-      CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<2>, kScanThreads, kScanSmem));
-    }
+    CKI(cudaFuncSetAttribute(k_scan<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem));
+    CKI(cudaFuncSetAttribute(k_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem));
+    CKI(cudaFuncSetAttribute(k_scan<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem));
+    CKI(cudaFuncSetAttribute(k_scan<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem));
+    if (c->cb == 1) CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<1>, kScanThreads, kScanSmem));
+    else CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<2>, kScanThreads, kScanSmem));
     c->scan_grid = std::max(1, occ) * c->sms;
     CKI(fold_occupancy(c->cb, c->lpa_log2, c->q_log2, &occ));
     c->fold_grid = std::max(1, occ) * c->sms;
@@ -451,7 +466,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
     rp.r = p.r; rp.u = p.u; rp.c = p.c; rp.W = c->W; rp.F = c->Fl;
     rp.z_base = c->z_base;
     rp.sys_fence = c->shard ? 1u : 0u;
-    rp.A_inv = c->A_inv; rp.g = p.g; rp.wpa = c->wpa; rp.theta = p.theta;
+    rp.A_inv = c->A_inv; rp.mangle_p = p.mangle; rp.g = p.g; rp.wpa = c->wpa; rp.theta = p.theta;
     rp.cells = (double)p.g * (double)c->E;
     rp.parts = (uint32_t)std::max<int>(1, std::min<int>(16, (2 * c->sms) / (int)c->Fl));
     std::vector<uint8_t> known(c->W, 0);
@@ -1056,7 +1071,7 @@ asse_status asse_get_clock(const void* ctx, uint64_t* t, uint32_t* C0) {
   return ASSE_OK;
 }
 
-asse_status asse_get_keys(const void* ctx, uint32_t* A, uint32_t* A_inv, uint64_t* K_bh) {
+asse_status asse_get_keys(const void* ctx, uint64_t* A, uint64_t* A_inv, uint64_t* K_bh) {
   if (!ctx) return ASSE_E_PARAM;
   const Ctx* c = static_cast<const Ctx*>(ctx);
   if (A) *A = c->A;

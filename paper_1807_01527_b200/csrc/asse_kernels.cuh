@@ -74,12 +74,36 @@ __device__ __forceinline__ void st_pool(uint4* p, uint4 v, uint64_t pol) {
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
 }
 
+// f(x) = A x mod p, p = 2^32 + 15 (the smallest prime above 2^32), with cycle walking
+// back into 32 bits (P:305 literal form). Reduction uses
+// 2^32 = -15 and 2^64 = 225 (mod p).
+constexpr uint64_t kMangleP = 4294967311ULL;
+__host__ __device__ __forceinline__ uint64_t mulmod_p(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+  const uint64_t lo = a * b, hi = __umul64hi(a, b);
+#else
+  const unsigned __int128 v = (unsigned __int128)a * b;
+  const uint64_t lo = (uint64_t)v, hi = (uint64_t)(v >> 64);
+#endif
+  int64_t t = (int64_t)(lo & 0xFFFFFFFFull) + (int64_t)(hi * 225u) - 15 * (int64_t)(lo >> 32)
+              + 16 * (int64_t)kMangleP;
+  const uint64_t u = (uint64_t)t;
+  int64_t t2 = (int64_t)(u & 0xFFFFFFFFull) - 15 * (int64_t)(u >> 32);
+  if (t2 < 0) t2 += (int64_t)kMangleP;
+  return (uint64_t)t2;
+}
+__host__ __device__ __forceinline__ uint32_t walk_mod_p(uint64_t key, uint32_t x) {
+  uint64_t y = mulmod_p(key, x);
+  while (y >> 32) y = mulmod_p(key, y);
+  return (uint32_t)y;
+}
+
 // ------------------------------------------------------------------- scan
 
 struct ScanParams {
   uint32_t* touch;        // touch bitmap, words_per_atv words per ATV
   uint64_t kbh;           // BH key
-  uint32_t A;             // mangling key (A8)
+  uint64_t A;             // mangling key (A8: odd, mod 2^32; or in [1, p-1] for MP)
   uint32_t g, r, u, c, W; // W = 32 - u
   uint32_t fmask, cmask;
   uint32_t wpa;           // touch words per ATV = g/32
@@ -88,9 +112,9 @@ struct ScanParams {
 
 // Alg. 3 for one pair: RRH(aip) -> r ATVs <x_y, y, z>, i = BH(bip),
 // SetAT recorded as touch bit i of each ATV.
-template <int CB>
+template <int CB, bool MP>
 __device__ __forceinline__ void scan_pair(const ScanParams& p, uint32_t aip, uint32_t bip) {
-  const uint32_t h = p.A * aip;                        // f(aip) = A*aip mod 2^32
+  const uint32_t h = MP ? walk_mod_p(p.A, aip) : (uint32_t)p.A * aip;   // f(aip)
   const uint32_t z = h & p.fmask;                      // Z(aip) = RBS(f, u)
   const uint64_t L = (uint64_t)(h >> p.u);             // LBS(f, 32-u)
   const uint64_t D = L | (L << p.W);                   // wrap-around view
@@ -118,7 +142,7 @@ constexpr size_t kScanSmem = (size_t)kScanStages * kScanTileBytes;
 // 4-stage shared-memory ring by bulk copies (TMA, cp.async.bulk; one producer warp),
 // tile i of this CTA = body tile blockIdx.x + i*gridDim.x; the 8 consumer warps
 // hash the packets and issue r RED.OR per packet into the L2-resident touch bitmap.
-template <int CB>
+template <int CB, bool MP = false>
 __global__ void __launch_bounds__(kScanThreads) k_scan(const uint2* __restrict__ pk, uint64_t n,
                                                        ScanParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -129,8 +153,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint2* __restrict__
   const uint64_t n_tiles = (body_bytes + kScanTileBytes - 1) / kScanTileBytes;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {     // scalar head / odd tail packets
-    if (head && n > 0) scan_pair<CB>(p, pk[0].x, pk[0].y);
-    if (nbody & 1) scan_pair<CB>(p, pk[n - 1].x, pk[n - 1].y);
+    if (head && n > 0) scan_pair<CB, MP>(p, pk[0].x, pk[0].y);
+    if (nbody & 1) scan_pair<CB, MP>(p, pk[n - 1].x, pk[n - 1].y);
   }
   const uint64_t my_tiles =
       (n_tiles > blockIdx.x) ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -165,8 +189,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint2* __restrict__
     const uint4* tp = reinterpret_cast<const uint4*>(smem + (size_t)st * kScanTileBytes);
     for (uint32_t q = threadIdx.x; q < n4; q += 32 * kScanConsumerWarps) {
       const uint4 v = tp[q];
-      scan_pair<CB>(p, v.x, v.y);
-      scan_pair<CB>(p, v.z, v.w);
+      scan_pair<CB, MP>(p, v.x, v.y);
+      scan_pair<CB, MP>(p, v.z, v.w);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -550,7 +574,9 @@ struct RestoreParams {
   void* reports;                 // asse_report per CSIP slot
   uint32_t* keys;                // ip per slot (device-wide sort)
   uint32_t* vals;                // slot index (device-wide sort)
-  uint32_t A_inv, g, wpa;
+  uint64_t A_inv;
+  uint32_t mangle_p;             // 1: f^{-1} by mod-p cycle walking
+  uint32_t g, wpa;
   uint32_t z_base;               // global index of local frame 0 (option S: rank * F_local)
   uint32_t sys_fence;            // option S: publish the reports to peers (system-scope fence)
   double theta, cells;           // cells = g * 2^c
@@ -692,7 +718,7 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
       if (nat == p.g) est = __longlong_as_double(0x7FF0000000000000LL);
       else est = -(double)p.g * log((double)(p.g - nat) / ((double)p.g * (1.0 - s_up)));
       const uint32_t flags = (nat == p.g ? 1u : 0u) | (est >= p.theta ? 2u : 0u);
-      const uint32_t ip = p.A_inv * h;
+      const uint32_t ip = p.mangle_p ? walk_mod_p(p.A_inv, h) : (uint32_t)p.A_inv * h;   // f^{-1}
       ReportDev* R = reinterpret_cast<ReportDev*>(p.reports) + slot;
       R->ip = ip; R->nat = nat; R->estimate = est; R->flags = flags; R->pad = 0;
       p.keys[slot] = ip;

@@ -111,6 +111,26 @@ def test_large_atv(cuda_device, g, k):
         step_both(dev, ora, gen.slice(t), geo["theta"], "g=%d k=%d t=%d" % (g, k, t))
 
 
+@pytest.mark.parametrize("name,N", [("C1", None), ("C3", 1_000_000)])
+def test_mod_p_mangling(cuda_device, name, N):
+    """the paper-literal mod-p mangling (config mangle = 1)."""
+    dev, ora, p = _pair(name, mangle=1)
+    assert dev.keys() == ora.keys()
+    g = Generator(name, N=N)
+    for t in range(4):
+        step_both(dev, ora, g.slice(t), p["theta"], "%s mod-p t=%d" % (name, t))
+    # hosts whose image A x mod p lands in [2^32, p) take the cycle walk on both sides
+    A, Ai, _ = ora.keys()
+    P = 2 ** 32 + 15
+    walkers = [x for x in ((Ai * t) % P for t in range(2 ** 32, P)) if x < 2 ** 32]
+    assert walkers
+    rng = np.random.default_rng(1)
+    rows = [np.stack([np.full(3000, x, np.uint64), rng.integers(0, 2 ** 32, 3000)], 1) for x in walkers]
+    pk = np.concatenate([g.slice(5, n=100_000).astype(np.uint64)] + rows).astype(np.uint32)
+    rd, ro = step_both(dev, ora, pk, p["theta"], "%s mod-p walkers" % name)
+    assert set(walkers) <= set(ro["ip"].tolist())
+
+
 def test_edge_cases_empty_ragged_misaligned_split(cuda_device):
     dev, ora, p = _pair("C1")
     g = Generator("C1")

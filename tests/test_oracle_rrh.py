@@ -123,3 +123,37 @@ def test_bh_uniform_and_deterministic():
     chi2 = float(((counts - exp) ** 2 / exp).sum())
     # df = 4095; mean 4095, sd ~ 90.5: accept within 5 sd
     assert abs(chi2 - 4095) < 5 * 90.5
+
+
+P_MANGLE = 2 ** 32 + 15   # the smallest prime above 2^32
+
+
+def test_mod_p_mangle_literal_form():
+    """f(aip) = A aip mod p with p prime > 2^32,
+    cycle-walked into 32 bits; checked against Python integers, A A^{-1} = 1 mod p,
+    and the round trip f^{-1}(f(x)) = x (including the digest/restore path)."""
+    geo = dict(PAPER_EX, mangle=1)
+    for seed in (1, 7, 2 ** 40 + 3):
+        o = O.Oracle(seed=seed, **geo)
+        A, Ai, _ = o.keys()
+        assert 1 <= A < P_MANGLE and (A * Ai) % P_MANGLE == 1
+        rng = np.random.default_rng(seed)
+        xs = rng.integers(0, 2 ** 32, 3000).tolist() + [0, 1, 2 ** 32 - 1]
+        for x in xs:
+            y = A * x % P_MANGLE
+            while y >= 2 ** 32:
+                y = A * y % P_MANGLE
+            assert o.mangle(x) == y
+            assert o.unmangle(y) == x
+            z, cols = o.digest(x)
+            assert o.restore_ip(o.restore_lbs(cols), z) == x
+    # a value whose image lands in [2^32, p) exercises the walk: search the inverse image
+    o = O.Oracle(seed=1, **geo)
+    A, Ai, _ = o.keys()
+    t = 2 ** 32 + 3                      # A x = t (mod p)  <=>  x = Ai t
+    x = Ai * t % P_MANGLE
+    if x < 2 ** 32:
+        y = A * t % P_MANGLE
+        while y >= 2 ** 32:
+            y = A * y % P_MANGLE
+        assert o.mangle(x) == y and o.unmangle(y) == x
