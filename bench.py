@@ -203,6 +203,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=20_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scan-variant", type=int, default=0, choices=[0, 1, 2],
+                    help="0 auto, 1 k_scan (direct RED.OR into L2), 2 k_scan_bin (shared-memory bins)")
     ap.add_argument("--replicated", action="store_true",
                     help="N>1: keep the whole pool on every GPU (option R) instead of frame sharding (S)")
     args = ap.parse_args()
@@ -239,6 +241,7 @@ def main():
     shard = 1 if (world > 1 and not args.replicated) else 0
     ctx = asse.Asse(**dict(p, world=world, rank=rank, device=local, max_candidates=1 << 20,
                            frame_shard=shard))
+    ctx.set_scan_variant(args.scan_variant)
     peers = attach_symmetric_peers(ctx) if world > 1 else None
     j0, stride, n_local = shard_slots(n_slice, rank, world)
 

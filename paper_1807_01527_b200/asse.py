@@ -21,7 +21,7 @@ _NAMES = {E_PARAM: "ASSE_E_PARAM", E_STATE: "ASSE_E_STATE", E_CAPACITY: "ASSE_E_
           E_OVERFLOW: "ASSE_E_OVERFLOW", E_CUDA: "ASSE_E_CUDA", E_PEER: "ASSE_E_PEER"}
 
 # every symbol include/asse.h declares
-SYMBOLS = ["asse_validate", "asse_init", "asse_destroy", "asse_last_error", "asse_set_timing",
+SYMBOLS = ["asse_validate", "asse_init", "asse_destroy", "asse_last_error", "asse_set_timing", "asse_set_scan_variant",
            "asse_scan_slice", "asse_scan_slice_host", "asse_end_slice", "asse_fetch_reports",
            "asse_export_pool", "asse_pool_size", "asse_get_clock", "asse_get_keys",
            "asse_get_stats", "asse_get_stream", "asse_attach_peers", "asse_bitmap_bytes",
@@ -55,7 +55,7 @@ class Stats(ctypes.Structure):
                 ("last_sort_ms", ctypes.c_double), ("last_end_slice_ms", ctypes.c_double),
                 ("last_n_super", ctypes.c_uint32), ("last_n_candidates", ctypes.c_uint32),
                 ("last_n_above", ctypes.c_uint32), ("w_theta", ctypes.c_uint32),
-                ("code_bytes", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
+                ("code_bytes", ctypes.c_uint32), ("scan_bin_launches", ctypes.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
@@ -80,6 +80,7 @@ def load_library(path=LIB_PATH):
         "asse_destroy": (None, [vp]),
         "asse_last_error": (ctypes.c_char_p, [vp]),
         "asse_set_timing": (i32, [vp, i32]),
+        "asse_set_scan_variant": (i32, [vp, i32]),
         "asse_scan_slice": (i32, [vp, vp, u64, vp]),
         "asse_scan_slice_host": (i32, [vp, vp, u64]),
         "asse_end_slice": (i32, [vp, vp, u32, ctypes.POINTER(u32), u32]),
@@ -157,6 +158,10 @@ class Asse:
 
     def set_timing(self, on=True):
         self._check(self._L.asse_set_timing(self._h, 1 if on else 0))
+
+    def set_scan_variant(self, variant):
+        """0 = automatic, 1 = k_scan (direct RED.OR), 2 = k_scan_bin (shared-memory bins)."""
+        self._check(self._L.asse_set_scan_variant(self._h, int(variant)))
 
     def scan_slice(self, pairs, n=None, stream=None):
         """pairs: device tensor (torch, uint32/int32, shape (n,2) or (2n,)) or a raw pointer."""

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -14,6 +16,7 @@
 
 #include "asse.h"
 #include "asse_kernels.cuh"
+#include "asse_scan_bin.cuh"
 
 using namespace asse;
 
@@ -44,6 +47,14 @@ struct Ctx {
   // device
   int device = 0, sms = 148;
   int scan_grid = 0, fold_grid = 0;   // resident CTAs (SMs x occupancy)
+  // binned scan (asse_scan_bin.cuh): one owner CTA per SM, shared-memory bitmap slices
+  int scan_variant = 0;               // 0 auto, 1 k_scan (direct RED), 2 k_scan_bin
+  bool bin_ok = false;                // geometry fits the SMs' shared memory
+  uint32_t bin_G = 0, bin_wpo = 0;
+  uint32_t bin_inv = 0;
+  size_t bin_smem = 0;
+  uint32_t* bin_queue = nullptr;      // [NB][G][QCAP]
+  uint32_t* bin_sync = nullptr;       // [2 NB]
   cudaStream_t stream = nullptr, copy_stream = nullptr;
   void* pool = nullptr;
   uint32_t* touch_own = nullptr;
@@ -167,7 +178,7 @@ static void free_all(Ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* dev[] = {c->pool, c->touch_own, c->active, c->scratch, c->sa_list, c->ws, c->cand, c->rep, c->rep_sorted, c->rep_above, c->keys,
                  c->keys_alt, c->vals, c->vals_alt, c->cub_tmp, c->export_buf, c->stage[0],
-                 c->stage[1]};
+                 c->stage[1], c->bin_queue, c->bin_sync};
   for (void* p : dev) if (p) cudaFree(p);
   if (c->h_counters) cudaFreeHost(c->h_counters);
   if (c->h_clock) cudaFreeHost(c->h_clock);
@@ -239,6 +250,73 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Binned scan (asse_scan_bin.cuh): cooperative launch (every CTA co-resident: they wait
+// on each other's rounds). Binned scans of every context in the process are serialized
+// on one event so that two such grids never share the GPU.
+static cudaEvent_t g_bin_last[64] = {nullptr};
+
+template <int CB, bool MP>
+static cudaError_t coop_launch_bin(Ctx* c, const uint2* pk, uint64_t n, const BinScanParams& bp, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(c->bin_G);
+  cfg.blockDim = dim3(kBinThreads);
+  cfg.dynamicSmemBytes = c->bin_smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_scan_bin<CB, MP>, pk, n, bp);
+}
+
+static asse_status launch_scan_bin(Ctx* c, const uint2* pk, uint64_t n, const ScanParams& sp, cudaStream_t st) {
+  const uint32_t G = c->bin_G;
+  if (!c->bin_queue) {
+    CK(cudaMalloc(&c->bin_queue, (size_t)kBinNB * G * kBinQG * kBinQCap * 4));
+    CK(cudaMalloc(&c->bin_sync, (2 * kBinNB + (size_t)kBinNB * G * kBinQG) * kBinPad * 4));
+  }
+  const int dev = c->device & 63;
+  if (!g_bin_last[dev]) CK(cudaEventCreateWithFlags(&g_bin_last[dev], cudaEventDisableTiming));
+  CK(cudaStreamWaitEvent(st, g_bin_last[dev], 0));
+  BinScanParams bp{};
+  bp.sp = sp;
+  bp.queue = c->bin_queue;
+  bp.qcnt = c->bin_sync + 2 * kBinNB * kBinPad;
+  bp.sync = c->bin_sync;
+  bp.total_words = c->n_atv_full * c->wpa;
+  bp.inv = c->bin_inv;
+  bp.wpo = c->bin_wpo;
+  static const bool prof = getenv("ASSE_SCAN_PROF") != nullptr;
+  if (prof) {
+    static unsigned long long* dprof = nullptr;
+    if (!dprof) CK(cudaMalloc(&dprof, 16 * 1024 * 8));
+    bp.prof = dprof;
+  }
+  CK(cudaMemsetAsync(c->bin_sync, 0, (2 * kBinNB + (size_t)kBinNB * G * kBinQG) * kBinPad * 4, st));
+  cudaError_t e;
+  if (c->cfg.mangle) e = c->cb == 1 ? coop_launch_bin<1, true>(c, pk, n, bp, st) : coop_launch_bin<2, true>(c, pk, n, bp, st);
+  else e = c->cb == 1 ? coop_launch_bin<1, false>(c, pk, n, bp, st) : coop_launch_bin<2, false>(c, pk, n, bp, st);
+  CK(e);
+  CK(cudaEventRecord(g_bin_last[dev], st));
+  if (bp.prof) {   // tools: ASSE_SCAN_PROF=1 prints per-phase cycles of the binned scan (syncs)
+    std::vector<unsigned long long> h((size_t)G * 16);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(h.data(), bp.prof, h.size() * 8, cudaMemcpyDeviceToHost));
+    const char* nm[13] = {"b_bin", "b_wait_reserve", "b_copy", "-", "-", "-",
+                          "-", "-", "-", "c0_wait", "c0_drain", "c1_wait", "c1_drain"};
+    fprintf(stderr, "k_scan_bin n=%llu G=%u:", (unsigned long long)n, G);
+    for (int q = 0; q < 13; ++q) {
+      double sum = 0, mx = 0;
+      for (uint32_t b = 0; b < G; ++b) { sum += (double)h[b * 16 + q]; mx = std::max(mx, (double)h[b * 16 + q]); }
+      fprintf(stderr, " %s %.0f/%.0f;", nm[q], sum / G, mx);
+    }
+    fprintf(stderr, "\n");
+  }
+  c->stats.scan_bin_launches++;
+  return ASSE_OK;
+}
+
 static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cudaStream_t st) {
   if (n == 0) return ASSE_OK;
   ScanParams p{};
@@ -250,7 +328,7 @@ static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cuda
   p.cmask = (1u << c->cfg.c) - 1u;
   p.wpa = c->wpa;
   for (int y = 0; y < kMaxR; ++y) p.shift[y] = c->shift[y];
-  const uint64_t tiles = ((n / 2) * 16 + kScanTileBytes - 1) / kScanTileBytes;
+  const uint64_t tiles = ((n / 2) * 16 + kScanTileBytes - 1) / kScanTileBytes;   // 16 KB tiles
   const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)c->scan_grid));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing) {
@@ -266,7 +344,12 @@ static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cuda
     CK(cudaEventRecord(e0, st));
   }
   const uint2* pk = reinterpret_cast<const uint2*>(d_pairs);
-  if (c->cfg.mangle) {
+  const bool use_bin = c->bin_ok && (c->scan_variant == 2 ||
+                                     (c->scan_variant == 0 && 2 * tiles >= (uint64_t)c->bin_G * kBinMinTilesPerCta));
+  if (use_bin) {
+    asse_status s = launch_scan_bin(c, pk, n, p, st);
+    if (s != ASSE_OK) return s;
+  } else if (c->cfg.mangle) {
     if (c->cb == 1) k_scan<1, true><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
     else k_scan<2, true><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
   } else {
@@ -438,6 +521,27 @@ asse_status asse_init(const asse_config* cfg, void** out) {
     if (c->cb == 1) CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<1>, kScanThreads, kScanSmem));
     else CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<2>, kScanThreads, kScanSmem));
     c->scan_grid = std::max(1, occ) * c->sms;
+    {
+      // binned scan: words per owner (multiple of 4) must fit next to the ring and bins
+      int optin = 0, coop = 0;
+      CKI(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+      CKI(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
+      const uint64_t words = c->n_atv_full * c->wpa;
+      c->bin_G = (uint32_t)c->sms;
+      c->bin_wpo = (uint32_t)(((words + c->bin_G - 1) / c->bin_G + 3) & ~3ull);
+      c->bin_inv = (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, ((1ull << 40) + c->bin_wpo - 1) / c->bin_wpo);
+      c->bin_smem = bin_smem_bytes(c->bin_G, c->bin_wpo);
+      c->bin_ok = coop && p.r == 4 && c->bin_wpo > 256 && (uint64_t)((c->bin_G + kBinQG - 1) / kBinQG) * kBinCap <= kBinQCap && (uint32_t)c->bin_G <= 32 * kBinBinWarps && words < (1ull << 25) && c->bin_wpo < (1u << 27) &&
+                  c->bin_smem + 2048 <= (size_t)optin;
+      if (c->bin_ok) {
+        void* fns[4] = {(void*)k_scan_bin<1, false>, (void*)k_scan_bin<2, false>, (void*)k_scan_bin<1, true>,
+                        (void*)k_scan_bin<2, true>};
+        for (void* f : fns) CKI(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->bin_smem));
+        int bocc = 0;
+        CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, k_scan_bin<1, false>, kBinThreads, c->bin_smem));
+        c->bin_ok = bocc >= 1;
+      }
+    }
     CKI(fold_occupancy(c->cb, c->lpa_log2, c->q_log2, &occ));
     c->fold_grid = std::max(1, occ) * c->sms;
   }
@@ -546,6 +650,15 @@ void asse_destroy(void* ctx) {
 asse_status asse_set_timing(void* ctx, int enable) {
   if (!ctx) return ASSE_E_PARAM;
   static_cast<Ctx*>(ctx)->timing = enable != 0;
+  return ASSE_OK;
+}
+
+asse_status asse_set_scan_variant(void* ctx, int variant) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (variant < 0 || variant > 2) { c->err = "scan variant is 0 (auto), 1 (direct) or 2 (binned)"; return ASSE_E_PARAM; }
+  if (variant == 2 && !c->bin_ok) { c->err = "binned scan unavailable for this geometry/device"; return ASSE_E_PARAM; }
+  c->scan_variant = variant;
   return ASSE_OK;
 }
 

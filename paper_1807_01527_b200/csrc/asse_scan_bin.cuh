@@ -1,0 +1,413 @@
+// asse_scan_bin.cuh — Alg. 3 with the touch bitmap held in shared memory.
+//
+// Why: k_scan issues r random 4-byte RED.OR per packet into the L2-resident touch
+// bitmap and runs at ~0.9 of the measured random-op ceiling (~188 Gop/s, 1.56
+// SM-cycles per update, tools/l2bench.cu). A random shared-memory atomic costs 0.18
+// SM-cycles and a coalesced 16-byte global access a small fraction of that
+// (tools/smembench.cu, profiles/). The bitmaps of the BASELINE geometries
+// (16 MiB at C3-C5) fit in the sum of the SMs' shared memories, so:
+//
+//  * one persistent CTA per SM (cooperative launch: all CTAs co-resident); CTA o OWNS
+//    touch words [o*wpo, (o+1)*wpo) and keeps them in shared memory for the whole call;
+//  * round t: every CTA takes one 16 KB packet tile (2048 packets, TMA bulk copy into a
+//    2-stage ring), computes the r SetAT targets of each packet exactly as k_scan does,
+//    and bins them by owner in shared memory (one shared atomic for the slot + a store);
+//  * it flushes bin o to its fixed slot [t mod NB][o][me] of a global queue (coalesced
+//    16-byte stores, L2-resident) and publishes the round with a release counter;
+//  * consumer warps of CTA o wait for round t to be published by every CTA and apply
+//    the entries addressed to it with shared-memory atomicOr;
+//  * at the end every CTA ORs its owned words into the global touch bitmap.
+//
+// A bin that overflows its CAP entries in one round falls back to a direct RED.OR of
+// the update into the global bitmap (same result: the write-back ORs). The state after
+// the call is bit-identical to k_scan's: the set of touch bits is a union, independent
+// of order (SetAT is idempotent within a slice).
+#pragma once
+#include "asse_kernels.cuh"
+
+namespace asse {
+
+constexpr int kBinBinWarps = 8;                            // binning + flushing warps
+constexpr int kBinConsWarps = 8;                           // queue-draining warps, two groups (round parity)
+constexpr int kBinConsWarp0 = kBinBinWarps;
+constexpr int kBinTmaWarp = kBinConsWarp0 + kBinConsWarps; // packet tiles -> shared ring (TMA)
+constexpr int kBinSigWarp = kBinTmaWarp + 1;               // publishes rounds (release fence off the
+                                                           // binning warps' path)
+constexpr int kBinThreads = 32 * (kBinSigWarp + 1);
+constexpr uint32_t kBinTileBytes = 8192;                   // 1024 packets per CTA per round
+constexpr int kBinRing = 4;                                // packet-tile ring stages
+constexpr int kBinCap = 64;                                // staged entries per (owner, round) in a CTA
+constexpr int kBinNB = 4;                                  // queue buffers (rounds) in flight
+constexpr uint32_t kBinQG = 4;                             // producer groups (CTA index mod 4) with separate
+                                                           // queues: 4x fewer reservations per counter
+constexpr uint32_t kBinQCap = 4096;                        // ring words per (buffer, owner, group)
+                                                           // >= ceil(G / QG) * kBinCap
+constexpr uint32_t kBinPad = 64;                           // words between counters: one 256-B L2 line
+                                                           // pair (one L2 slice) per counter
+constexpr uint32_t kBinMinTilesPerCta = 8;                 // below: k_scan is used
+
+struct BinScanParams {
+  ScanParams sp;          // hashing parameters and the global touch bitmap
+  uint32_t* queue;        // [NB][G owners][QG][QCAP] rings of entries (local word << 5 | bit)
+  uint32_t* qcnt;         // [NB][G owners][QG] x kBinPad: entries ever reserved (monotone per launch)
+  uint32_t* sync;         // [2 NB] x kBinPad: rounds published per buffer, then rounds drained; zeroed
+                          // per launch
+  uint64_t total_words;   // words of the touch bitmap
+  uint32_t inv;           // ceil(2^40 / wpo) (< 2^32 for wpo > 256): owner = (w * inv) >> 40, exact for
+                          // w < 2^25 (the error term w * (inv - 2^40/wpo) / 2^40 < 1/wpo)
+  uint32_t wpo;           // touch words per owner (multiple of 4)
+  unsigned long long* prof;  // optional per-CTA phase cycle counters [G][16] (tools; may be null)
+};
+
+__host__ __device__ constexpr size_t bin_smem_bytes(uint32_t G, uint32_t wpo) {
+  return (size_t)kBinRing * kBinTileBytes + 2 * (size_t)G * kBinCap * 4 + 2 * (((size_t)G * 4 + 15) & ~(size_t)15) +
+         (size_t)wpo * 4;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Poll a monotone counter (relaxed: the data it guards is read with L2-coherent .cg loads
+// issued after the poll returns; the writer published it with a release fence).
+__device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t target) {
+  while (ld_relaxed_gpu(p) < target) __nanosleep(64);   // polls must not steal issue slots
+}
+// mbarrier wait for warps off the critical path (sleeps between probes)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+    if (done) break;
+    __nanosleep(128);
+  }
+}
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" :: "r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// shared-space (32-bit address) accessors: no generic-to-shared conversion per access
+__device__ __forceinline__ uint32_t atoms_inc(uint32_t addr) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(addr) : "memory");
+  return old;
+}
+// bin slot = old value of the owner's counter; 0 (no access) when !pred
+__device__ __forceinline__ uint32_t atoms_inc_if(bool pred, uint32_t addr) {
+  uint32_t old;
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n mov.u32 %0, 0;\n"
+               " @p atom.shared.add.u32 %0, [%2], 1;\n}"
+               : "=r"(old) : "r"((uint32_t)pred), "r"(addr) : "memory");
+  return old;
+}
+__device__ __forceinline__ void sts_if(bool pred, uint32_t addr, uint32_t v) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.shared.u32 [%1], %2;\n}"
+               :: "r"((uint32_t)pred), "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_or_if(bool pred, uint32_t* gaddr, uint32_t v) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p red.global.or.b32 [%1], %2;\n}"
+               :: "r"((uint32_t)pred), "l"(gaddr), "r"(v) : "memory");
+}
+
+// The 4 SetAT targets (touch words) of one packet (identical arithmetic to scan_pair;
+// the binned kernel serves r = 4, the rows of every BASELINE geometry).
+template <int CB, bool MP>
+__device__ __forceinline__ void targets4(const ScanParams& p, uint32_t aip, uint32_t bip, uint32_t* w,
+                                         uint32_t& tb) {
+  const uint32_t h = MP ? walk_mod_p(p.A, aip) : (uint32_t)p.A * aip;   // f(aip)
+  const uint32_t z = h & p.fmask;                                         // Z
+  const uint64_t L = (uint64_t)(h >> p.u);                                // LBS
+  const uint64_t D = L | (L << p.W);                                      // wrap-around
+  const uint32_t i = bh_index(bip, p.kbh, p.g);                           // BH (A13)
+  const uint32_t wofs = i >> 5;
+  tb = touch_bit<CB>(i);
+  const uint32_t yz0 = z << p.c;
+#pragma unroll
+  for (int y = 0; y < 4; ++y) {
+    const uint32_t x = (uint32_t)(D >> p.shift[y]) & p.cmask;
+    const uint32_t atv = ((uint32_t)y << (p.u + p.c)) + yz0 + x;
+    w[y] = atv * p.wpa + wofs;
+  }
+}
+
+// Bin the 8 updates of two packets: 8 independent shared atomics for the bin slots, then
+// predicated stores. A full bin (rare) sends its update straight to the global bitmap.
+// Called by whole warps (the overflow vote is warp-wide); lanes with !valid do nothing.
+template <int CB, bool MP>
+__device__ __forceinline__ void bin_two(const BinScanParams& bp, const uint4 v, bool valid, uint32_t stg_s,
+                                        uint32_t scount_s) {
+  uint32_t w[8], tb0, tb1;
+  targets4<CB, MP>(bp.sp, v.x, v.y, w, tb0);
+  targets4<CB, MP>(bp.sp, v.z, v.w, w + 4, tb1);
+  uint32_t o[8], pos[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) o[k] = (uint32_t)(((uint64_t)w[k] * bp.inv) >> 40);   // one IMAD.WIDE
+#pragma unroll
+  for (int k = 0; k < 8; ++k) pos[k] = atoms_inc_if(valid, scount_s + 4u * o[k]);
+  uint32_t ovf = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t tb = k < 4 ? tb0 : tb1;
+    const uint32_t e = ((w[k] - o[k] * bp.wpo) << 5) | tb;
+    const bool ok = pos[k] < (uint32_t)kBinCap;
+    sts_if(valid && ok, stg_s + 4u * (o[k] * kBinCap + pos[k]), e);
+    ovf |= (valid && !ok ? 1u : 0u) << k;
+  }
+  if (__any_sync(0xffffffffu, ovf != 0)) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (ovf & (1u << k)) atomicOr(bp.sp.touch + w[k], 1u << (k < 4 ? tb0 : tb1));
+  }
+}
+
+template <int CB, bool MP = false>
+__global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __restrict__ pk, uint64_t n,
+                                                             BinScanParams bp) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int kSig = 8;
+  static_assert(kSig > kBinNB + 1, "signal barrier ring");
+  __shared__ __align__(8) uint64_t full[kBinRing], empty[kBinRing], sigbar[kSig];
+  const uint32_t G = gridDim.x, me = blockIdx.x;
+  const uint32_t Gp = (G + 3u) & ~3u;
+  uint8_t* ring = smem;
+  uint32_t* stg = reinterpret_cast<uint32_t*>(smem + (size_t)kBinRing * kBinTileBytes);  // [2][G][CAP]
+  uint32_t* scount = stg + 2 * (size_t)G * kBinCap;                                      // [2][Gp]
+  uint32_t* sbm = scount + 2 * Gp;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t head = (((uintptr_t)pk) & 15u) ? 1u : 0u;
+  const uint64_t nbody = (n > head) ? n - head : 0;
+  const uint64_t body_bytes = (nbody >> 1) * 16u;
+  const uint64_t n_tiles = (body_bytes + kBinTileBytes - 1) / kBinTileBytes;
+  const uint32_t R = (uint32_t)((n_tiles + G - 1) / G);        // rounds; tile of CTA b in round t: t*G + b
+  uint32_t* prod_done = bp.sync;                 // counter of buffer b at b * kBinPad
+  uint32_t* cons_done = bp.sync + kBinNB * kBinPad;
+  constexpr int kBinT = 32 * kBinBinWarps;                    // named barrier 1
+  constexpr int kGroupThreads = 32 * (kBinConsWarps / 2);     // named barriers 2, 3
+  constexpr int kComputeThreads = 32 * (kBinBinWarps + kBinConsWarps);   // named barrier 4
+
+  for (uint32_t q = threadIdx.x; q < bp.wpo; q += blockDim.x) sbm[q] = 0;
+  for (uint32_t q = threadIdx.x; q < 2 * Gp; q += blockDim.x) scount[q] = 0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kBinRing; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kBinBinWarps);
+    }
+    for (int q = 0; q < kSig; ++q) mbar_init(&sigbar[q], kBinBinWarps);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const uint8_t* body = reinterpret_cast<const uint8_t*>(pk + head);
+
+  if (warp == kBinSigWarp) {                     // ---------------- round publication
+    // the binning warps run at most NB + 1 rounds ahead of this warp (they wait for rounds
+    // NB back to be drained, which needs them published), so kSig > NB + 1 barriers suffice
+    for (uint32_t tf = 0; tf < R; ++tf) {
+      mbar_wait_sleep(&sigbar[tf % kSig], (tf / kSig) & 1u);   // every binning warp wrote round tf
+      if (lane == 0) {
+        __threadfence();                         // cumulative release of those writes
+        atomicAdd(prod_done + (tf % kBinNB) * kBinPad, 1u);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  if (warp == kBinTmaWarp) {                     // ---------------- packet tiles -> ring
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t i = 0;
+      for (uint32_t t = 0; t < R; ++t) {
+        const uint64_t tile = (uint64_t)t * G + me;
+        if (tile >= n_tiles) break;
+        const uint32_t st = i % kBinRing;
+        if (i >= (uint32_t)kBinRing) mbar_wait_sleep(&empty[st], ((i / kBinRing) - 1) & 1u);
+        const uint64_t off = tile * (uint64_t)kBinTileBytes;
+        const uint32_t bytes = (uint32_t)umin64(kBinTileBytes, body_bytes - off);
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(ring + (size_t)st * kBinTileBytes, body + off, bytes, &full[st], pol);
+        ++i;
+      }
+    }
+    return;
+  }
+
+  if (warp < (uint32_t)kBinBinWarps) {           // ---------------- binning + flushing warps
+    const uint32_t tid = threadIdx.x;
+    if (me == 0 && tid == 0) {                   // scalar head / odd tail packets: direct RED
+      if (head && n > 0) scan_pair<CB, MP>(bp.sp, pk[0].x, pk[0].y);
+      if (nbody & 1) scan_pair<CB, MP>(bp.sp, pk[n - 1].x, pk[n - 1].y);
+    }
+    uint32_t i = 0;
+    unsigned long long pc[3] = {0, 0, 0};
+    long long c0 = clock64(), c1;
+    // iteration t: reserve queue space for round t-1 (staging (t-1)&1), bin round t into
+    // staging t&1 (hiding the reservation latency), copy round t-1 into the reserved ranges.
+    // Owners of this warp: o = warp + kBinBinWarps * l for lanes l with o < G.
+    const uint32_t my_o = warp + kBinBinWarps * lane;
+    for (uint32_t t = 0; t <= R; ++t) {
+      const uint32_t sb = t & 1u, sf = sb ^ 1u;
+      const uint32_t tf = t - 1, bf = tf % kBinNB;
+      uint32_t cnt = 0, off = 0;
+      if (t >= 1) {
+        if (tid == 0 && tf >= (uint32_t)kBinNB) spin_until_geq(cons_done + bf * kBinPad, G * (tf / kBinNB));
+        named_bar(1, kBinT);                     // round tf-NB drained everywhere: its qcnt read
+        if (my_o < G) {
+          cnt = min(scount[sf * Gp + my_o], (uint32_t)kBinCap);
+          if (cnt) off = atomicAdd(bp.qcnt + (((size_t)bf * G + my_o) * kBinQG + (me % kBinQG)) * kBinPad, cnt);
+        }
+      }
+      c1 = clock64(); pc[1] += c1 - c0; c0 = c1;
+      if (t < R) {
+        const uint64_t tile = (uint64_t)t * G + me;
+        if (tile < n_tiles) {
+          const uint32_t st = i % kBinRing;
+          mbar_wait(&full[st], (i / kBinRing) & 1u);
+          const uint32_t n4 = (uint32_t)umin64(kBinTileBytes, body_bytes - tile * (uint64_t)kBinTileBytes) >> 4;
+          const uint4* tp = reinterpret_cast<const uint4*>(ring + (size_t)st * kBinTileBytes);
+          const uint32_t stg_s = smem_u32(stg + (size_t)sb * G * kBinCap), scount_s = smem_u32(scount + sb * Gp);
+          for (uint32_t q0 = tid - lane; q0 < n4; q0 += kBinT) {   // warp-uniform trip count
+            const uint32_t q = q0 + lane;
+            const bool valid = q < n4;
+            bin_two<CB, MP>(bp, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
+          ++i;
+        }
+      }
+      c1 = clock64(); pc[0] += c1 - c0; c0 = c1;
+      if (t >= 1) {
+        const uint32_t* stg_f = stg + (size_t)sf * G * kBinCap;
+        uint32_t* qb = bp.queue + ((size_t)bf * G * kBinQG + (me % kBinQG)) * kBinQCap;
+        const uint32_t nown = (G - warp + kBinBinWarps - 1) / kBinBinWarps;
+        // owner l of this warp: entries q = lane and lane + 32 (cnt <= 64); batches of 4
+        // owners with every shared load issued before the global stores
+        uint32_t src_s = smem_u32(stg_f + (size_t)warp * kBinCap) + 4u * lane;
+        uint32_t* dst = qb + (size_t)warp * kBinQG * kBinQCap;
+        constexpr uint32_t kSrcStep = kBinBinWarps * kBinCap * 4;          // bytes between owners
+        constexpr size_t kDstStep = (size_t)kBinBinWarps * kBinQG * kBinQCap;
+        constexpr int UB = 4;
+        for (uint32_t l0 = 0; l0 < nown; l0 += UB) {
+          uint32_t c[UB], of[UB], v0[UB], v1[UB];
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            c[u] = __shfl_sync(0xffffffffu, cnt, l0 + u);     // 0 for owners beyond nown
+            of[u] = __shfl_sync(0xffffffffu, off, l0 + u) + lane;
+            const uint32_t a = src_s + u * kSrcStep;
+            asm volatile("{\n .reg .pred p;\n setp.lt.u32 p, %2, %3;\n mov.u32 %0, 0;\n"
+                         " @p ld.shared.u32 %0, [%1];\n}" : "=r"(v0[u]) : "r"(a), "r"(lane), "r"(c[u]));
+            asm volatile("{\n .reg .pred p;\n setp.lt.u32 p, %2, %3;\n mov.u32 %0, 0;\n"
+                         " @p ld.shared.u32 %0, [%1+128];\n}" : "=r"(v1[u]) : "r"(a), "r"(lane + 32), "r"(c[u]));
+          }
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            uint32_t* dp = dst + u * kDstStep;
+            if (lane < c[u]) dp[of[u] & (kBinQCap - 1)] = v0[u];
+            if (lane + 32 < c[u]) dp[(of[u] + 32) & (kBinQCap - 1)] = v1[u];
+          }
+          src_s += UB * kSrcStep;
+          dst += UB * kDstStep;
+        }
+        if (my_o < G) scount[sf * Gp + my_o] = 0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sigbar[tf % kSig]);   // this warp wrote round tf (release.cta)
+        named_bar(1, kBinT);                     // staging sf and its counts reusable
+      }
+      c1 = clock64(); pc[2] += c1 - c0; c0 = c1;
+    }
+    if (bp.prof && tid == 0)
+      for (int q = 0; q < 3; ++q) bp.prof[me * 16 + q] = pc[q];
+  } else {                                       // ---------------- queue-draining warps
+    const uint32_t cid = warp - kBinConsWarp0;
+    const uint32_t grp = cid / (kBinConsWarps / 2);
+    const uint32_t gtid = threadIdx.x - 32 * (kBinConsWarp0 + grp * (kBinConsWarps / 2));
+    constexpr uint32_t GT = 32 * (kBinConsWarps / 2);
+    uint32_t last[2][kBinQG];                    // this group's buffers b = grp and grp + 2
+#pragma unroll
+    for (int g = 0; g < (int)kBinQG; ++g) last[0][g] = last[1][g] = 0;
+    unsigned long long cwait = 0, cwork = 0;
+    long long c0 = clock64(), c1;
+    for (uint32_t t = grp; t < R; t += 2) {
+      const uint32_t b = t % kBinNB, li = (t >> 1) & 1u;
+      if (gtid == 0) spin_until_geq(prod_done + b * kBinPad, G * (t / kBinNB + 1));
+      named_bar(2 + grp, kGroupThreads);
+      c1 = clock64(); cwait += c1 - c0; c0 = c1;
+      // the round's entries: QG ranges [last, end) of the owner's rings, drained as one list
+      uint32_t st[kBinQG], pre[kBinQG + 1];
+      pre[0] = 0;
+#pragma unroll
+      for (int g = 0; g < (int)kBinQG; ++g) {
+        const uint32_t end = ld_cg_u32(bp.qcnt + (((size_t)b * G + me) * kBinQG + g) * kBinPad);
+        const uint32_t s0 = li ? last[1][g] : last[0][g];
+        st[g] = s0;
+        pre[g + 1] = pre[g] + (end - s0);
+        if (li) last[1][g] = end; else last[0][g] = end;
+      }
+      const uint32_t* qb = bp.queue + ((size_t)b * G + me) * kBinQG * kBinQCap;
+      uint32_t len[kBinQG], mx = 0;
+#pragma unroll
+      for (int g = 0; g < (int)kBinQG; ++g) { len[g] = pre[g + 1] - pre[g]; mx = max(mx, len[g]); }
+      constexpr int U = 4;                       // entries in flight per thread per group ring
+      for (uint32_t e0 = gtid; e0 < mx; e0 += U * GT) {
+        uint32_t v[kBinQG][U];
+#pragma unroll
+        for (int g = 0; g < (int)kBinQG; ++g)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t e = e0 + u * GT;
+            v[g][u] = (e < len[g]) ? ld_cg_u32(qb + g * kBinQCap + ((st[g] + e) & (kBinQCap - 1))) : 0xFFFFFFFFu;
+          }
+#pragma unroll
+        for (int g = 0; g < (int)kBinQG; ++g)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (v[g][u] != 0xFFFFFFFFu) atomicOr(sbm + (v[g][u] >> 5), 1u << (v[g][u] & 31u));
+      }
+      named_bar(2 + grp, kGroupThreads);
+      if (gtid == 0) atomicAdd(cons_done + b * kBinPad, 1u);   // entries consumed (values used) before
+      c1 = clock64(); cwork += c1 - c0; c0 = c1;
+    }
+    if (bp.prof && gtid == 0) { bp.prof[me * 16 + 9 + 2 * grp] = cwait; bp.prof[me * 16 + 10 + 2 * grp] = cwork; }
+  }
+  // every round consumed by this CTA: every producer has published every round, so all
+  // overflow REDs are performed; OR the owned words into the global bitmap
+  named_bar(4, kComputeThreads);
+  const uint64_t w0 = (uint64_t)me * bp.wpo;
+  if (w0 < bp.total_words) {
+    const uint32_t nw = (uint32_t)umin64(bp.wpo, bp.total_words - w0);
+    uint4* gdst = reinterpret_cast<uint4*>(bp.sp.touch + w0);
+    const uint4* ssrc = reinterpret_cast<const uint4*>(sbm);
+    for (uint32_t q = threadIdx.x; q < (nw >> 2); q += kComputeThreads) {
+      const uint4 s = ssrc[q];
+      if (s.x | s.y | s.z | s.w) {
+        uint4 gv;
+        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(gv.x), "=r"(gv.y), "=r"(gv.z), "=r"(gv.w) : "l"(gdst + q));
+        gv.x |= s.x; gv.y |= s.y; gv.z |= s.z; gv.w |= s.w;
+        gdst[q] = gv;
+      }
+    }
+  }
+}
+
+}  // namespace asse
