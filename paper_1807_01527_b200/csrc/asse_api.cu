@@ -531,7 +531,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
       c->bin_wpo = (uint32_t)(((words + c->bin_G - 1) / c->bin_G + 3) & ~3ull);
       c->bin_inv = (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, ((1ull << 40) + c->bin_wpo - 1) / c->bin_wpo);
       c->bin_smem = bin_smem_bytes(c->bin_G, c->bin_wpo);
-      c->bin_ok = coop && p.r == 4 && c->bin_wpo > 256 && (uint64_t)((c->bin_G + kBinQG - 1) / kBinQG) * kBinCap <= kBinQCap && (uint32_t)c->bin_G <= 32 * kBinBinWarps && words < (1ull << 25) && c->bin_wpo < (1u << 27) &&
+      c->bin_ok = coop && p.r == 4 && c->bin_wpo > 256 && (uint64_t)((c->bin_G + kBinQG - 1) / kBinQG) * kBinCap <= kBinQCap && (uint32_t)c->bin_G <= kMaxOwners && words < (1ull << 25) && c->bin_wpo < (1u << 27) &&
                   c->bin_smem + 2048 <= (size_t)optin;
       if (c->bin_ok) {
         void* fns[4] = {(void*)k_scan_bin<1, false>, (void*)k_scan_bin<2, false>, (void*)k_scan_bin<1, true>,

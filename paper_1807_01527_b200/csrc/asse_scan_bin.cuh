@@ -27,7 +27,7 @@
 
 namespace asse {
 
-constexpr int kBinBinWarps = 8;                            // binning + flushing warps
+constexpr int kBinBinWarps = 16;                           // binning + flushing warps
 constexpr int kBinConsWarps = 8;                           // queue-draining warps, two groups (round parity)
 constexpr int kBinConsWarp0 = kBinBinWarps;
 constexpr int kBinTmaWarp = kBinConsWarp0 + kBinConsWarps; // packet tiles -> shared ring (TMA)
@@ -37,6 +37,9 @@ constexpr int kBinThreads = 32 * (kBinSigWarp + 1);
 constexpr uint32_t kBinTileBytes = 8192;                   // 1024 packets per CTA per round
 constexpr int kBinRing = 4;                                // packet-tile ring stages
 constexpr int kBinCap = 64;                                // staged entries per (owner, round) in a CTA
+constexpr int kBinStride = 68;                             // words between bins: bin o starts at bank
+                                                           // 4o mod 32, so equal slots of different bins
+                                                           // do not collide (16-B aligned)
 constexpr int kBinNB = 4;                                  // queue buffers (rounds) in flight
 constexpr uint32_t kBinQG = 4;                             // producer groups (CTA index mod 4) with separate
                                                            // queues: 4x fewer reservations per counter
@@ -45,6 +48,7 @@ constexpr uint32_t kBinQCap = 4096;                        // ring words per (bu
 constexpr uint32_t kBinPad = 64;                           // words between counters: one 256-B L2 line
                                                            // pair (one L2 slice) per counter
 constexpr uint32_t kBinMinTilesPerCta = 8;                 // below: k_scan is used
+constexpr uint32_t kMaxOwners = 160;                       // owners (SMs) the kernel is built for
 
 struct BinScanParams {
   ScanParams sp;          // hashing parameters and the global touch bitmap
@@ -60,7 +64,7 @@ struct BinScanParams {
 };
 
 __host__ __device__ constexpr size_t bin_smem_bytes(uint32_t G, uint32_t wpo) {
-  return (size_t)kBinRing * kBinTileBytes + 2 * (size_t)G * kBinCap * 4 + 2 * (((size_t)G * 4 + 15) & ~(size_t)15) +
+  return (size_t)kBinRing * kBinTileBytes + 2 * (size_t)G * kBinStride * 4 + 2 * (((size_t)G * 4 + 15) & ~(size_t)15) +
          (size_t)wpo * 4;
 }
 
@@ -171,7 +175,7 @@ __device__ __forceinline__ void bin_two(const BinScanParams& bp, const uint4 v, 
     const uint32_t tb = k < 4 ? tb0 : tb1;
     const uint32_t e = ((w[k] - o[k] * bp.wpo) << 5) | tb;
     const bool ok = pos[k] < (uint32_t)kBinCap;
-    sts_if(valid && ok, stg_s + 4u * (o[k] * kBinCap + pos[k]), e);
+    sts_if(valid && ok, stg_s + 4u * (o[k] * kBinStride + pos[k]), e);
     ovf |= (valid && !ok ? 1u : 0u) << k;
   }
   if (__any_sync(0xffffffffu, ovf != 0)) {
@@ -191,8 +195,8 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
   const uint32_t G = gridDim.x, me = blockIdx.x;
   const uint32_t Gp = (G + 3u) & ~3u;
   uint8_t* ring = smem;
-  uint32_t* stg = reinterpret_cast<uint32_t*>(smem + (size_t)kBinRing * kBinTileBytes);  // [2][G][CAP]
-  uint32_t* scount = stg + 2 * (size_t)G * kBinCap;                                      // [2][Gp]
+  uint32_t* stg = reinterpret_cast<uint32_t*>(smem + (size_t)kBinRing * kBinTileBytes);  // [2][G][STRIDE]
+  uint32_t* scount = stg + 2 * (size_t)G * kBinStride;                                   // [2][Gp]
   uint32_t* sbm = scount + 2 * Gp;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint32_t head = (((uintptr_t)pk) & 15u) ? 1u : 0u;
@@ -268,15 +272,23 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
       const uint32_t sb = t & 1u, sf = sb ^ 1u;
       const uint32_t tf = t - 1, bf = tf % kBinNB;
       uint32_t cnt = 0, off = 0;
+      // the end-of-iteration barrier (below) made staging sf final and queue buffer bf free
       if (t >= 1) {
-        if (tid == 0 && tf >= (uint32_t)kBinNB) spin_until_geq(cons_done + bf * kBinPad, G * (tf / kBinNB));
-        named_bar(1, kBinT);                     // round tf-NB drained everywhere: its qcnt read
         if (my_o < G) {
-          cnt = min(scount[sf * Gp + my_o], (uint32_t)kBinCap);
+          // whole 16-B groups: pad the bin with "no entry" words up to a multiple of 4
+          const uint32_t c = min(scount[sf * Gp + my_o], (uint32_t)kBinCap);
+          cnt = (c + 3u) & ~3u;
+          uint32_t* bin = stg + ((size_t)sf * G + my_o) * kBinStride;
+          for (uint32_t q = c; q < cnt; ++q) bin[q] = 0xFFFFFFFFu;
           if (cnt) off = atomicAdd(bp.qcnt + (((size_t)bf * G + my_o) * kBinQG + (me % kBinQG)) * kBinPad, cnt);
         }
       }
       c1 = clock64(); pc[1] += c1 - c0; c0 = c1;
+      // the drain count the next reservation (round t into buffer t % NB) waits for, loaded
+      // early so its latency hides behind the binning
+      uint32_t seen = 0;
+      const uint32_t need = G * (t / kBinNB);
+      if (tid == 0 && t >= (uint32_t)kBinNB && t < R) seen = ld_relaxed_gpu(cons_done + (t % kBinNB) * kBinPad);
       if (t < R) {
         const uint64_t tile = (uint64_t)t * G + me;
         if (tile < n_tiles) {
@@ -284,7 +296,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
           mbar_wait(&full[st], (i / kBinRing) & 1u);
           const uint32_t n4 = (uint32_t)umin64(kBinTileBytes, body_bytes - tile * (uint64_t)kBinTileBytes) >> 4;
           const uint4* tp = reinterpret_cast<const uint4*>(ring + (size_t)st * kBinTileBytes);
-          const uint32_t stg_s = smem_u32(stg + (size_t)sb * G * kBinCap), scount_s = smem_u32(scount + sb * Gp);
+          const uint32_t stg_s = smem_u32(stg + (size_t)sb * G * kBinStride), scount_s = smem_u32(scount + sb * Gp);
           for (uint32_t q0 = tid - lane; q0 < n4; q0 += kBinT) {   // warp-uniform trip count
             const uint32_t q = q0 + lane;
             const bool valid = q < n4;
@@ -297,42 +309,37 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
       }
       c1 = clock64(); pc[0] += c1 - c0; c0 = c1;
       if (t >= 1) {
-        const uint32_t* stg_f = stg + (size_t)sf * G * kBinCap;
+        const uint32_t* stg_f = stg + (size_t)sf * G * kBinStride;
         uint32_t* qb = bp.queue + ((size_t)bf * G * kBinQG + (me % kBinQG)) * kBinQCap;
-        const uint32_t nown = (G - warp + kBinBinWarps - 1) / kBinBinWarps;
-        // owner l of this warp: entries q = lane and lane + 32 (cnt <= 64); batches of 4
-        // owners with every shared load issued before the global stores
-        uint32_t src_s = smem_u32(stg_f + (size_t)warp * kBinCap) + 4u * lane;
-        uint32_t* dst = qb + (size_t)warp * kBinQG * kBinQCap;
-        constexpr uint32_t kSrcStep = kBinBinWarps * kBinCap * 4;          // bytes between owners
-        constexpr size_t kDstStep = (size_t)kBinBinWarps * kBinQG * kBinQCap;
-        constexpr int UB = 4;
-        for (uint32_t l0 = 0; l0 < nown; l0 += UB) {
-          uint32_t c[UB], of[UB], v0[UB], v1[UB];
+        // two owners per step (one per half-warp), 16 B per lane: staged bin -> ring; all
+        // shared loads of the warp's owners are issued before the global stores
+        const uint32_t hl = lane & 15u, hw = lane >> 4;
+        const uint32_t src_s = smem_u32(stg_f + (size_t)(warp + kBinBinWarps * hw) * kBinStride) + 16u * hl;
+        uint4* dst = reinterpret_cast<uint4*>(qb + (size_t)(warp + kBinBinWarps * hw) * kBinQG * kBinQCap);
+        constexpr uint32_t kSrcStep = 2 * kBinBinWarps * kBinStride * 4;    // bytes between steps
+        constexpr size_t kDstStep = 2 * (size_t)kBinBinWarps * kBinQG * kBinQCap / 4;
+        constexpr int NS = (kMaxOwners + 2 * kBinBinWarps - 1) / (2 * kBinBinWarps);   // steps
+        uint4 v[NS];
+        uint32_t c4[NS], of[NS];
 #pragma unroll
-          for (int u = 0; u < UB; ++u) {
-            c[u] = __shfl_sync(0xffffffffu, cnt, l0 + u);     // 0 for owners beyond nown
-            of[u] = __shfl_sync(0xffffffffu, off, l0 + u) + lane;
-            const uint32_t a = src_s + u * kSrcStep;
-            asm volatile("{\n .reg .pred p;\n setp.lt.u32 p, %2, %3;\n mov.u32 %0, 0;\n"
-                         " @p ld.shared.u32 %0, [%1];\n}" : "=r"(v0[u]) : "r"(a), "r"(lane), "r"(c[u]));
-            asm volatile("{\n .reg .pred p;\n setp.lt.u32 p, %2, %3;\n mov.u32 %0, 0;\n"
-                         " @p ld.shared.u32 %0, [%1+128];\n}" : "=r"(v1[u]) : "r"(a), "r"(lane + 32), "r"(c[u]));
-          }
-#pragma unroll
-          for (int u = 0; u < UB; ++u) {
-            uint32_t* dp = dst + u * kDstStep;
-            if (lane < c[u]) dp[of[u] & (kBinQCap - 1)] = v0[u];
-            if (lane + 32 < c[u]) dp[(of[u] + 32) & (kBinQCap - 1)] = v1[u];
-          }
-          src_s += UB * kSrcStep;
-          dst += UB * kDstStep;
+        for (int k = 0; k < NS; ++k) {
+          c4[k] = __shfl_sync(0xffffffffu, cnt, 2 * k + hw);   // 0 beyond nown
+          of[k] = __shfl_sync(0xffffffffu, off, 2 * k + hw);
+          const uint32_t a = src_s + k * kSrcStep;
+          if (4 * hl < c4[k])
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w) : "r"(a));
         }
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+          if (4 * hl < c4[k]) dst[k * kDstStep + (((of[k] >> 2) + hl) & (kBinQCap / 4 - 1))] = v[k];
         if (my_o < G) scount[sf * Gp + my_o] = 0;
         __syncwarp();
         if (lane == 0) mbar_arrive(&sigbar[tf % kSig]);   // this warp wrote round tf (release.cta)
-        named_bar(1, kBinT);                     // staging sf and its counts reusable
       }
+      if (tid == 0 && t >= (uint32_t)kBinNB && t < R && seen < need)
+        spin_until_geq(cons_done + (t % kBinNB) * kBinPad, need);   // round t-NB drained everywhere
+      named_bar(1, kBinT);                       // bins of round t final; staging sf and counts reusable
       c1 = clock64(); pc[2] += c1 - c0; c0 = c1;
     }
     if (bp.prof && tid == 0)
@@ -367,21 +374,32 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
       uint32_t len[kBinQG], mx = 0;
 #pragma unroll
       for (int g = 0; g < (int)kBinQG; ++g) { len[g] = pre[g + 1] - pre[g]; mx = max(mx, len[g]); }
-      constexpr int U = 4;                       // entries in flight per thread per group ring
-      for (uint32_t e0 = gtid; e0 < mx; e0 += U * GT) {
-        uint32_t v[kBinQG][U];
+      constexpr int U = 2;                       // 16-B groups in flight per thread per ring
+      const uint4* qb4 = reinterpret_cast<const uint4*>(qb);
+      for (uint32_t e0 = gtid; 4 * e0 < mx; e0 += U * GT) {
+        uint4 v[kBinQG][U];
 #pragma unroll
         for (int g = 0; g < (int)kBinQG; ++g)
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const uint32_t e = e0 + u * GT;
-            v[g][u] = (e < len[g]) ? ld_cg_u32(qb + g * kBinQCap + ((st[g] + e) & (kBinQCap - 1))) : 0xFFFFFFFFu;
+            const uint32_t e = e0 + u * GT;      // 16-B group index within the round's range
+            v[g][u] = make_uint4(~0u, ~0u, ~0u, ~0u);
+            if (4 * e < len[g]) {
+              const uint4* a = qb4 + g * (kBinQCap / 4) + (((st[g] >> 2) + e) & (kBinQCap / 4 - 1));
+              asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(v[g][u].x), "=r"(v[g][u].y), "=r"(v[g][u].z), "=r"(v[g][u].w) : "l"(a));
+            }
           }
 #pragma unroll
         for (int g = 0; g < (int)kBinQG; ++g)
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (v[g][u] != 0xFFFFFFFFu) atomicOr(sbm + (v[g][u] >> 5), 1u << (v[g][u] & 31u));
+          for (int u = 0; u < U; ++u) {
+            const uint4 x = v[g][u];
+            if (x.x != ~0u) atomicOr(sbm + (x.x >> 5), 1u << (x.x & 31u));
+            if (x.y != ~0u) atomicOr(sbm + (x.y >> 5), 1u << (x.y & 31u));
+            if (x.z != ~0u) atomicOr(sbm + (x.z >> 5), 1u << (x.z & 31u));
+            if (x.w != ~0u) atomicOr(sbm + (x.w >> 5), 1u << (x.w & 31u));
+          }
       }
       named_bar(2 + grp, kGroupThreads);
       if (gtid == 0) atomicAdd(cons_done + b * kBinPad, 1u);   // entries consumed (values used) before
