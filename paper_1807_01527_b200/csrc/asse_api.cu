@@ -50,7 +50,7 @@ struct Ctx {
   // binned scan (asse_scan_bin.cuh): one owner CTA per SM, shared-memory bitmap slices
   int scan_variant = 0;               // 0 auto, 1 k_scan (direct RED), 2 k_scan_bin
   bool bin_ok = false;                // geometry fits the SMs' shared memory
-  uint32_t bin_G = 0, bin_wpo = 0;
+  uint32_t bin_G = 0, bin_wpo = 0, bin_rr = 1, bin_tile = 0;   // rows via RED (measured best: 1), tile bytes
   uint32_t bin_inv = 0;
   size_t bin_smem = 0;
   uint32_t* bin_queue = nullptr;      // [NB][G][QCAP]
@@ -255,7 +255,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 // on one event so that two such grids never share the GPU.
 static cudaEvent_t g_bin_last[64] = {nullptr};
 
-template <int CB, bool MP>
+template <int CB, bool MP, int RR>
 static cudaError_t coop_launch_bin(Ctx* c, const uint2* pk, uint64_t n, const BinScanParams& bp, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(c->bin_G);
@@ -267,7 +267,13 @@ static cudaError_t coop_launch_bin(Ctx* c, const uint2* pk, uint64_t n, const Bi
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_scan_bin<CB, MP>, pk, n, bp);
+  return cudaLaunchKernelEx(&cfg, k_scan_bin<CB, MP, RR>, pk, n, bp);
+}
+template <int CB, bool MP>
+static cudaError_t coop_launch_bin_rr(Ctx* c, const uint2* pk, uint64_t n, const BinScanParams& bp, cudaStream_t st) {
+  if (c->bin_rr == 0) return coop_launch_bin<CB, MP, 0>(c, pk, n, bp, st);
+  if (c->bin_rr == 1) return coop_launch_bin<CB, MP, 1>(c, pk, n, bp, st);
+  return coop_launch_bin<CB, MP, 2>(c, pk, n, bp, st);
 }
 
 static asse_status launch_scan_bin(Ctx* c, const uint2* pk, uint64_t n, const ScanParams& sp, cudaStream_t st) {
@@ -284,7 +290,10 @@ static asse_status launch_scan_bin(Ctx* c, const uint2* pk, uint64_t n, const Sc
   bp.queue = c->bin_queue;
   bp.qcnt = c->bin_sync + 2 * kBinNB * kBinPad;
   bp.sync = c->bin_sync;
-  bp.total_words = c->n_atv_full * c->wpa;
+  const uint64_t row_words = (uint64_t)c->F * c->E * c->wpa;
+  bp.base_word = (uint32_t)(c->bin_rr * row_words);
+  bp.total_words = c->n_atv_full * c->wpa - bp.base_word;
+  bp.tile_bytes = c->bin_tile;
   bp.inv = c->bin_inv;
   bp.wpo = c->bin_wpo;
   static const bool prof = getenv("ASSE_SCAN_PROF") != nullptr;
@@ -295,8 +304,8 @@ static asse_status launch_scan_bin(Ctx* c, const uint2* pk, uint64_t n, const Sc
   }
   CK(cudaMemsetAsync(c->bin_sync, 0, (2 * kBinNB + (size_t)kBinNB * G * kBinQG) * kBinPad * 4, st));
   cudaError_t e;
-  if (c->cfg.mangle) e = c->cb == 1 ? coop_launch_bin<1, true>(c, pk, n, bp, st) : coop_launch_bin<2, true>(c, pk, n, bp, st);
-  else e = c->cb == 1 ? coop_launch_bin<1, false>(c, pk, n, bp, st) : coop_launch_bin<2, false>(c, pk, n, bp, st);
+  if (c->cfg.mangle) e = c->cb == 1 ? coop_launch_bin_rr<1, true>(c, pk, n, bp, st) : coop_launch_bin_rr<2, true>(c, pk, n, bp, st);
+  else e = c->cb == 1 ? coop_launch_bin_rr<1, false>(c, pk, n, bp, st) : coop_launch_bin_rr<2, false>(c, pk, n, bp, st);
   CK(e);
   CK(cudaEventRecord(g_bin_last[dev], st));
   if (bp.prof) {   // tools: ASSE_SCAN_PROF=1 prints per-phase cycles of the binned scan (syncs)
@@ -345,7 +354,7 @@ static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cuda
   }
   const uint2* pk = reinterpret_cast<const uint2*>(d_pairs);
   const bool use_bin = c->bin_ok && (c->scan_variant == 2 ||
-                                     (c->scan_variant == 0 && 2 * tiles >= (uint64_t)c->bin_G * kBinMinTilesPerCta));
+                                     (c->scan_variant == 0 && tiles * kScanTileBytes >= (uint64_t)c->bin_G * kBinMinTilesPerCta * c->bin_tile));
   if (use_bin) {
     asse_status s = launch_scan_bin(c, pk, n, p, st);
     if (s != ASSE_OK) return s;
@@ -526,19 +535,28 @@ asse_status asse_init(const asse_config* cfg, void** out) {
       int optin = 0, coop = 0;
       CKI(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
       CKI(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
-      const uint64_t words = c->n_atv_full * c->wpa;
+      // rows below bin_rr take the direct RED route, the rest are binned (ASSE_SCAN_RR
+      // overrides, tools only); 4096 binned updates per CTA per round
+      if (const char* e = getenv("ASSE_SCAN_RR")) c->bin_rr = (uint32_t)std::min(2, std::max(0, atoi(e)));
+      const uint64_t row_words = (uint64_t)c->F * c->E * c->wpa;
       c->bin_G = (uint32_t)c->sms;
+      if (((p.r - c->bin_rr) * row_words) / c->bin_G <= 256) c->bin_rr = 0;   // small geometries: bin all rows
+      const uint64_t words = (p.r - c->bin_rr) * row_words;
+      c->bin_tile = (uint32_t)((4096 / (4 - c->bin_rr)) * 8 / 16 * 16);
       c->bin_wpo = (uint32_t)(((words + c->bin_G - 1) / c->bin_G + 3) & ~3ull);
       c->bin_inv = (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, ((1ull << 40) + c->bin_wpo - 1) / c->bin_wpo);
-      c->bin_smem = bin_smem_bytes(c->bin_G, c->bin_wpo);
-      c->bin_ok = coop && p.r == 4 && c->bin_wpo > 256 && (uint64_t)((c->bin_G + kBinQG - 1) / kBinQG) * kBinCap <= kBinQCap && (uint32_t)c->bin_G <= kMaxOwners && words < (1ull << 25) && c->bin_wpo < (1u << 27) &&
+      c->bin_smem = bin_smem_bytes(c->bin_G, c->bin_wpo, c->bin_tile);
+      c->bin_ok = coop && p.r == 4 && c->bin_wpo > 256 && (uint64_t)((c->bin_G + kBinQG - 1) / kBinQG) * kBinCap <= kBinQCap &&
+                  (uint32_t)c->bin_G <= kMaxOwners && words < (1ull << 25) && c->bin_wpo < (1u << 27) &&
                   c->bin_smem + 2048 <= (size_t)optin;
       if (c->bin_ok) {
-        void* fns[4] = {(void*)k_scan_bin<1, false>, (void*)k_scan_bin<2, false>, (void*)k_scan_bin<1, true>,
-                        (void*)k_scan_bin<2, true>};
+        void* fns[12] = {(void*)k_scan_bin<1, false, 0>, (void*)k_scan_bin<2, false, 0>, (void*)k_scan_bin<1, true, 0>,
+                         (void*)k_scan_bin<2, true, 0>, (void*)k_scan_bin<1, false, 1>, (void*)k_scan_bin<2, false, 1>,
+                         (void*)k_scan_bin<1, true, 1>, (void*)k_scan_bin<2, true, 1>, (void*)k_scan_bin<1, false, 2>,
+                         (void*)k_scan_bin<2, false, 2>, (void*)k_scan_bin<1, true, 2>, (void*)k_scan_bin<2, true, 2>};
         for (void* f : fns) CKI(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->bin_smem));
         int bocc = 0;
-        CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, k_scan_bin<1, false>, kBinThreads, c->bin_smem));
+        CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, k_scan_bin<1, false, 2>, kBinThreads, c->bin_smem));
         c->bin_ok = bocc >= 1;
       }
     }

@@ -34,7 +34,6 @@ constexpr int kBinTmaWarp = kBinConsWarp0 + kBinConsWarps; // packet tiles -> sh
 constexpr int kBinSigWarp = kBinTmaWarp + 1;               // publishes rounds (release fence off the
                                                            // binning warps' path)
 constexpr int kBinThreads = 32 * (kBinSigWarp + 1);
-constexpr uint32_t kBinTileBytes = 8192;                   // 1024 packets per CTA per round
 constexpr int kBinRing = 4;                                // packet-tile ring stages
 constexpr int kBinCap = 64;                                // staged entries per (owner, round) in a CTA
 constexpr int kBinStride = 68;                             // words between bins: bin o starts at bank
@@ -56,16 +55,18 @@ struct BinScanParams {
   uint32_t* qcnt;         // [NB][G owners][QG] x kBinPad: entries ever reserved (monotone per launch)
   uint32_t* sync;         // [2 NB] x kBinPad: rounds published per buffer, then rounds drained; zeroed
                           // per launch
-  uint64_t total_words;   // words of the touch bitmap
+  uint64_t total_words;   // binned words: rows RR..r-1 of the touch bitmap
+  uint32_t base_word;     // first binned word (RR rows x 2^(u+c) ATVs x g/32 words)
+  uint32_t tile_bytes;    // packets per CTA per round x 8 (4096 binned updates per round)
   uint32_t inv;           // ceil(2^40 / wpo) (< 2^32 for wpo > 256): owner = (w * inv) >> 40, exact for
                           // w < 2^25 (the error term w * (inv - 2^40/wpo) / 2^40 < 1/wpo)
   uint32_t wpo;           // touch words per owner (multiple of 4)
   unsigned long long* prof;  // optional per-CTA phase cycle counters [G][16] (tools; may be null)
 };
 
-__host__ __device__ constexpr size_t bin_smem_bytes(uint32_t G, uint32_t wpo) {
-  return (size_t)kBinRing * kBinTileBytes + 2 * (size_t)G * kBinStride * 4 + 2 * (((size_t)G * 4 + 15) & ~(size_t)15) +
-         (size_t)wpo * 4;
+__host__ __device__ constexpr size_t bin_smem_bytes(uint32_t G, uint32_t wpo, uint32_t tile_bytes) {
+  return (size_t)kBinRing * tile_bytes + 2 * (size_t)G * kBinStride * 4 + 2 * (((size_t)G * 4 + 15) & ~(size_t)15) +
+         16 + (size_t)wpo * 4;
 }
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
@@ -86,7 +87,7 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
 // Poll a monotone counter (relaxed: the data it guards is read with L2-coherent .cg loads
 // issued after the poll returns; the writer published it with a release fence).
 __device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t target) {
-  while (ld_relaxed_gpu(p) < target) __nanosleep(64);   // polls must not steal issue slots
+  while (ld_relaxed_gpu(p) < target) __nanosleep(128);   // polls must not steal issue slots
 }
 // mbarrier wait for warps off the critical path (sleeps between probes)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
@@ -98,7 +99,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
         " selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
     if (done) break;
-    __nanosleep(128);
+    __nanosleep(256);
   }
 }
 __device__ __forceinline__ void named_bar(int id, int threads) {
@@ -157,37 +158,50 @@ __device__ __forceinline__ void targets4(const ScanParams& p, uint32_t aip, uint
 
 // Bin the 8 updates of two packets: 8 independent shared atomics for the bin slots, then
 // predicated stores. A full bin (rare) sends its update straight to the global bitmap.
-// Called by whole warps (the overflow vote is warp-wide); lanes with !valid do nothing.
-template <int CB, bool MP>
+// Rows y < RR of both packets go straight to the global bitmap (RED.OR into L2, k_scan's
+// route); rows y >= RR are binned: RR balances the L2 random-op path against the SMs'
+// binning work. Called by whole warps (the overflow vote is warp-wide); lanes with !valid
+// do nothing.
+template <int CB, bool MP, int RR>
 __device__ __forceinline__ void bin_two(const BinScanParams& bp, const uint4 v, bool valid, uint32_t stg_s,
-                                        uint32_t scount_s) {
+                                        uint32_t scount_s, uint32_t scount_dummy) {
   uint32_t w[8], tb0, tb1;
   targets4<CB, MP>(bp.sp, v.x, v.y, w, tb0);
   targets4<CB, MP>(bp.sp, v.z, v.w, w + 4, tb1);
-  uint32_t o[8], pos[8];
+  constexpr int NB2 = 4 - RR;                    // binned updates per packet
 #pragma unroll
-  for (int k = 0; k < 8; ++k) o[k] = (uint32_t)(((uint64_t)w[k] * bp.inv) >> 40);   // one IMAD.WIDE
+  for (int k = 0; k < 8; ++k)
+    if ((k & 3) < RR) red_or_if(valid, bp.sp.touch + w[k], 1u << (k < 4 ? tb0 : tb1));
+  uint32_t o[2 * NB2], pos[2 * NB2], wl[2 * NB2];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) pos[k] = atoms_inc_if(valid, scount_s + 4u * o[k]);
+  for (int m = 0; m < 2 * NB2; ++m) {
+    const int k = (m / NB2) * 4 + RR + (m % NB2);
+    wl[m] = w[k] - bp.base_word;
+    o[m] = (uint32_t)(((uint64_t)wl[m] * bp.inv) >> 40);   // one IMAD.WIDE
+  }
+  // lanes without a packet count into a spare counter (index G) instead of branching
+#pragma unroll
+  for (int m = 0; m < 2 * NB2; ++m) pos[m] = atoms_inc(valid ? scount_s + 4u * o[m] : scount_dummy);
   uint32_t ovf = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t tb = k < 4 ? tb0 : tb1;
-    const uint32_t e = ((w[k] - o[k] * bp.wpo) << 5) | tb;
-    const bool ok = pos[k] < (uint32_t)kBinCap;
-    sts_if(valid && ok, stg_s + 4u * (o[k] * kBinStride + pos[k]), e);
-    ovf |= (valid && !ok ? 1u : 0u) << k;
+  for (int m = 0; m < 2 * NB2; ++m) {
+    const uint32_t tb = m < NB2 ? tb0 : tb1;
+    const uint32_t e = ((wl[m] - o[m] * bp.wpo) << 5) | tb;
+    const bool ok = pos[m] < (uint32_t)kBinCap;
+    sts_if(valid && ok, stg_s + 4u * (o[m] * kBinStride + pos[m]), e);
+    ovf |= (valid && !ok ? 1u : 0u) << m;
   }
   if (__any_sync(0xffffffffu, ovf != 0)) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (ovf & (1u << k)) atomicOr(bp.sp.touch + w[k], 1u << (k < 4 ? tb0 : tb1));
+    for (int m = 0; m < 2 * NB2; ++m)
+      if (ovf & (1u << m)) atomicOr(bp.sp.touch + bp.base_word + wl[m], 1u << (m < NB2 ? tb0 : tb1));
   }
 }
 
-template <int CB, bool MP = false>
+template <int CB, bool MP, int RR>
 __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __restrict__ pk, uint64_t n,
                                                              BinScanParams bp) {
+  const uint32_t kBinTileBytes = bp.tile_bytes;
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int kSig = 8;
   static_assert(kSig > kBinNB + 1, "signal barrier ring");
@@ -197,7 +211,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
   uint8_t* ring = smem;
   uint32_t* stg = reinterpret_cast<uint32_t*>(smem + (size_t)kBinRing * kBinTileBytes);  // [2][G][STRIDE]
   uint32_t* scount = stg + 2 * (size_t)G * kBinStride;                                   // [2][Gp]
-  uint32_t* sbm = scount + 2 * Gp;
+  uint32_t* sbm = scount + 2 * Gp + 4;           // 4 spare words: dummy bin counter
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint32_t head = (((uintptr_t)pk) & 15u) ? 1u : 0u;
   const uint64_t nbody = (n > head) ? n - head : 0;
@@ -300,7 +314,8 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
           for (uint32_t q0 = tid - lane; q0 < n4; q0 += kBinT) {   // warp-uniform trip count
             const uint32_t q = q0 + lane;
             const bool valid = q < n4;
-            bin_two<CB, MP>(bp, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s);
+            bin_two<CB, MP, RR>(bp, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s,
+                            smem_u32(scount + 2 * Gp));
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[st]);
@@ -413,7 +428,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
   const uint64_t w0 = (uint64_t)me * bp.wpo;
   if (w0 < bp.total_words) {
     const uint32_t nw = (uint32_t)umin64(bp.wpo, bp.total_words - w0);
-    uint4* gdst = reinterpret_cast<uint4*>(bp.sp.touch + w0);
+    uint4* gdst = reinterpret_cast<uint4*>(bp.sp.touch + bp.base_word + w0);
     const uint4* ssrc = reinterpret_cast<const uint4*>(sbm);
     for (uint32_t q = threadIdx.x; q < (nw >> 2); q += kComputeThreads) {
       const uint4 s = ssrc[q];
