@@ -84,6 +84,8 @@ typedef struct {
   uint32_t w_theta;              /* integer super-ATV weight threshold (A15) */
   uint32_t code_bytes;           /* device AT code width: 1 or 2 (A2) */
   uint32_t scan_bin_launches;    /* cumulative launches of the binned scan (k_scan_bin) */
+  uint32_t scan_rows_red;        /* k_scan_bin: rows whose SetATs take the direct RED route */
+  uint32_t scan_bin_ok;          /* 1 if k_scan_bin is available for this geometry/device */
 } asse_stats;
 
 /* Validate a configuration (completeness/redundancy P:315-324, A10; the device
@@ -104,11 +106,11 @@ const char* asse_last_error(const void* ctx);
 /* Enable/disable per-kernel CUDA-event timing (asse_stats.*_ms). Default off. */
 asse_status asse_set_timing(void* ctx, int enable);
 
-/* Scan kernel selection: 0 = automatic (default: the binned shared-memory scan
- * k_scan_bin when the touch bitmap fits the SMs' shared memory and a call brings at
- * least 4 packet tiles of 2048 packets per SM, else k_scan), 1 = always k_scan (one
- * RED.OR per SetAT into the L2-resident bitmap), 2 = always k_scan_bin (ASSE_E_PARAM
- * if the geometry does not fit). Both produce the identical touch bitmap. */
+/* Scan kernel selection: 0 = automatic (default: the binned scan k_scan_bin when its
+ * part of the touch bitmap fits the SMs' shared memory, r = 4, and a call brings at least
+ * 8 rounds of packets per SM, else k_scan), 1 = always k_scan (one RED.OR per SetAT into
+ * the L2-resident bitmap), 2 = always k_scan_bin (ASSE_E_PARAM if unavailable). Both
+ * produce the identical touch bitmap (SetAT is idempotent). */
 asse_status asse_set_scan_variant(void* ctx, int variant);
 
 /* Alg. 3 "Scan IP pair" for n_pairs packets of the current slice.

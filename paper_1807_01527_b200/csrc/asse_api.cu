@@ -559,6 +559,8 @@ asse_status asse_init(const asse_config* cfg, void** out) {
         CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, k_scan_bin<1, false, 2>, kBinThreads, c->bin_smem));
         c->bin_ok = bocc >= 1;
       }
+      c->stats.scan_rows_red = c->bin_rr;
+      c->stats.scan_bin_ok = c->bin_ok ? 1u : 0u;
     }
     CKI(fold_occupancy(c->cb, c->lpa_log2, c->q_log2, &occ));
     c->fold_grid = std::max(1, occ) * c->sms;
