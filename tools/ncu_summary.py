@@ -26,6 +26,10 @@ METRICS = [
     "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
     "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+    "sm__inst_issued.avg.pct_of_peak_sustained_active", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed_op_shared_atom.sum",
+    "lts__t_sectors_op_read.sum", "lts__t_sectors_op_write.sum", "lts__t_sectors_op_red.sum",
 ]
 
 
@@ -98,15 +102,20 @@ def main():
                 if m in d:
                     md.append("- `%s` = %s" % (m, d[m]))
             md.append("")
-        scans = [d for d in res if d["kernel"].endswith("k_scan<1>") or "k_scan" in d["kernel"]]
+        scans = [d for d in res if "k_scan" in d["kernel"]]
         if scans:
             d = scans[0]
-            mb = num(d["dram__bytes_read.sum"]) * (1 if "Mbyte" in d["dram__bytes_read.sum"] else 1e-6 if "byte" in d["dram__bytes_read.sum"].split()[1] and "M" not in d["dram__bytes_read.sum"] else 1)
-            wb = num(d["dram__bytes_write.sum"]) * (1 if "Mbyte" in d["dram__bytes_write.sum"] else 1e-3 if "Kbyte" in d["dram__bytes_write.sum"] else 1)
+            scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+            def mbytes(v):
+                x, u = v.split()[0], v.split()[1]
+                return float(x.replace(",", "")) * scale[u]
+            mb, wb = mbytes(d["dram__bytes_read.sum"]), mbytes(d["dram__bytes_write.sum"])
             per = (mb + wb) * 1e6 / a.packets
+            kname = d["kernel"].split("::")[-1].split("<")[0]
             with open(os.path.join(a.out, "scan_traffic.json"), "w") as f:
-                json.dump({"source": "%s k_scan ncu --set full" % a.tag, "packets_per_launch": a.packets,
-                           "dram_bytes_per_launch": (mb + wb) * 1e6, "dram_bytes_per_packet": per}, f, indent=1)
+                json.dump({"source": "%s %s ncu --set full" % (a.tag, d["kernel"]), "kernel": kname,
+                           "packets_per_launch": a.packets, "dram_bytes_per_launch": (mb + wb) * 1e6,
+                           "dram_bytes_per_packet": per}, f, indent=1)
     with open(os.path.join(a.out, "%s_ncu_summary.md" % a.tag), "w") as f:
         f.write("\n".join(md) + "\n")
     with open(os.path.join(a.out, "%s_ncu_summary.json" % a.tag), "w") as f:
