@@ -86,11 +86,11 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
 }
 // Poll a monotone counter (relaxed: the data it guards is read with L2-coherent .cg loads
 // issued after the poll returns; the writer published it with a release fence).
-__device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t target) {
-  while (ld_relaxed_gpu(p) < target) __nanosleep(128);   // polls must not steal issue slots
+__device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t target, uint32_t ns = 128) {
+  while (ld_relaxed_gpu(p) < target) __nanosleep(ns);   // polls must not steal issue slots
 }
 // mbarrier wait for warps off the critical path (sleeps between probes)
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, uint32_t ns) {
   uint32_t done = 0;
   while (true) {
     asm volatile(
@@ -99,7 +99,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
         " selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
     if (done) break;
-    __nanosleep(256);
+    __nanosleep(ns);
   }
 }
 __device__ __forceinline__ void named_bar(int id, int threads) {
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
     // the binning warps run at most NB + 1 rounds ahead of this warp (they wait for rounds
     // NB back to be drained, which needs them published), so kSig > NB + 1 barriers suffice
     for (uint32_t tf = 0; tf < R; ++tf) {
-      mbar_wait_sleep(&sigbar[tf % kSig], (tf / kSig) & 1u);   // every binning warp wrote round tf
+      mbar_wait_sleep(&sigbar[tf % kSig], (tf / kSig) & 1u, 400);   // every binning warp wrote round tf
       if (lane == 0) {
         __threadfence();                         // cumulative release of those writes
         atomicAdd(prod_done + (tf % kBinNB) * kBinPad, 1u);
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
         const uint64_t tile = (uint64_t)t * G + me;
         if (tile >= n_tiles) break;
         const uint32_t st = i % kBinRing;
-        if (i >= (uint32_t)kBinRing) mbar_wait_sleep(&empty[st], ((i / kBinRing) - 1) & 1u);
+        if (i >= (uint32_t)kBinRing) mbar_wait_sleep(&empty[st], ((i / kBinRing) - 1) & 1u, 1000);
         const uint64_t off = tile * (uint64_t)kBinTileBytes;
         const uint32_t bytes = (uint32_t)umin64(kBinTileBytes, body_bytes - off);
         mbar_expect_tx(&full[st], bytes);
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
     long long c0 = clock64(), c1;
     for (uint32_t t = grp; t < R; t += 2) {
       const uint32_t b = t % kBinNB, li = (t >> 1) & 1u;
-      if (gtid == 0) spin_until_geq(prod_done + b * kBinPad, G * (t / kBinNB + 1));
+      if (gtid == 0) spin_until_geq(prod_done + b * kBinPad, G * (t / kBinNB + 1), 300);
       named_bar(2 + grp, kGroupThreads);
       c1 = clock64(); cwait += c1 - c0; c0 = c1;
       // the round's entries: QG ranges [last, end) of the owner's rings, drained as one list
