@@ -255,12 +255,21 @@ def main():
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream())
 
-    def step(t):
-        ctx.scan_slice(bufs[t % S])
-        return ctx.end_slice(0)
+    # one step = one slice, pipelined: the slice's scan is queued behind the previous
+    # slice's end_slice (asse_end_slice_async), whose results are read while it runs
+    def run(t0, t1, on_result=None):
+        for t in range(t0, t1):
+            ctx.scan_slice(bufs[t % S])
+            if t > t0:
+                rep = ctx.end_slice_wait()
+                if on_result:
+                    on_result(rep)
+            ctx.end_slice_async(0)
+        rep = ctx.end_slice_wait()
+        if on_result:
+            on_result(rep)
 
-    for t in range(args.warmup):
-        step(t)
+    run(0, args.warmup)
     ctx.set_timing(True)
     st0 = ctx.stats()
     end_ms, scan_ms_steps = [], []
@@ -272,13 +281,14 @@ def main():
         n_rep = 0
         phases = {k: [] for k in ("last_merge_ms", "last_fold_ms", "last_restore_ms", "last_nat_ms",
                                   "last_sort_ms")}
-        for t in range(args.warmup, args.warmup + args.steps):
-            rep = step(t)
+        def on_result(rep):
+            nonlocal n_rep
             n_rep += len(rep)
             s = ctx.stats()
             end_ms.append(s["last_end_slice_ms"])
             for k in phases:
                 phases[k].append(s[k])
+        run(args.warmup, args.warmup + args.steps, on_result)
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -314,8 +324,10 @@ def main():
         t0 = time.perf_counter()
         for t in range(args.steps):
             ctx.scan_slice_host(host[t % 2])
-            rep = ctx.end_slice(0)
-            d2h += rep.nbytes + 32
+            if t:
+                d2h += ctx.end_slice_wait().nbytes + 32
+            ctx.end_slice_async(0)
+        d2h += ctx.end_slice_wait().nbytes + 32
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0)
         barrier()

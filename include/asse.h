@@ -142,6 +142,22 @@ asse_status asse_scan_slice_host(void* ctx, const uint32_t* h_pairs, uint64_t n_
 asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out,
                            uint32_t mode);
 
+/* Asynchronous asse_end_slice, for pipelining slices: enqueues everything asse_end_slice
+ * does (merge, fold, restore, NAT/Eq. 5, sort, the copy of the counters and of a report
+ * prefix to pinned host memory) on the context's stream and returns at once. The slice
+ * counts as closed on return (t+1, C0 advanced), so the next slice's asse_scan_slice may
+ * be issued before its results are read; the device runs the scans after this slice's
+ * kernels (stream order). At most one slice may be pending: asse_end_slice_wait must be
+ * called before the next asse_end_slice(_async), query, fetch, export, save/load or merge
+ * (those return ASSE_E_STATE meanwhile). Errors of the slice itself (ASSE_E_OVERFLOW,
+ * ASSE_E_CAPACITY) are reported by asse_end_slice_wait. */
+asse_status asse_end_slice_async(void* ctx, uint32_t mode);
+
+/* Wait for the pending asynchronous end_slice and return its reports with the same
+ * conventions as asse_end_slice (h_out caller-owned host array of cap reports, *n_out
+ * produced; mode was given to asse_end_slice_async). ASSE_E_STATE if none is pending. */
+asse_status asse_end_slice_wait(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out);
+
 /* Window query (checkAT for any k' <= k): super
  * points and Eq. 5 estimates over the k_prime slices ending at the last closed slice,
  * evaluated on the current pool without modifying it. 1 <= k_prime < k (the advance's

@@ -26,7 +26,8 @@ SYMBOLS = ["asse_validate", "asse_init", "asse_destroy", "asse_last_error", "ass
            "asse_export_pool", "asse_pool_size", "asse_get_clock", "asse_get_keys",
            "asse_get_stats", "asse_get_stream", "asse_attach_peers", "asse_bitmap_bytes",
            "asse_merge", "asse_query_window", "asse_save_state", "asse_load_state",
-           "asse_merged_bytes", "asse_exchange_bytes", "asse_end_slice_begin"]
+           "asse_merged_bytes", "asse_exchange_bytes", "asse_end_slice_begin", "asse_end_slice_async",
+           "asse_end_slice_wait"]
 
 
 class AsseError(RuntimeError):
@@ -85,6 +86,8 @@ def load_library(path=LIB_PATH):
         "asse_scan_slice": (i32, [vp, vp, u64, vp]),
         "asse_scan_slice_host": (i32, [vp, vp, u64]),
         "asse_end_slice": (i32, [vp, vp, u32, ctypes.POINTER(u32), u32]),
+        "asse_end_slice_async": (i32, [vp, u32]),
+        "asse_end_slice_wait": (i32, [vp, vp, u32, ctypes.POINTER(u32)]),
         "asse_fetch_reports": (i32, [vp, vp, u32, ctypes.POINTER(u32), u32]),
         "asse_export_pool": (i32, [vp, vp, u64]),
         "asse_pool_size": (u64, [vp]),
@@ -204,6 +207,25 @@ class Asse:
     def end_slice(self, mode=1):
         """Close the slice; returns the reports (numpy REPORT_DTYPE, ascending ip)."""
         return self._call_reports(self._L.asse_end_slice, mode)
+
+    def end_slice_async(self, mode=1):
+        """Close the slice without waiting for its results (asse_end_slice_async); the
+        next slice's scan_slice may follow at once. Read them with end_slice_wait()."""
+        self._check(self._L.asse_end_slice_async(self._h, mode))
+        self._pend_mode = mode
+
+    def end_slice_wait(self):
+        """Reports of the pending asynchronous end_slice."""
+        n = ctypes.c_uint32()
+        cap = max(self._cap, 1024)
+        buf = np.empty(cap, dtype=REPORT_DTYPE)
+        st = self._L.asse_end_slice_wait(self._h, buf.ctypes.data, cap, ctypes.byref(n))
+        if st == E_CAPACITY and n.value > cap:
+            self._cap = n.value
+            return self._call_reports(self._L.asse_fetch_reports, self._pend_mode)
+        self._check(st)
+        self._cap = max(self._cap, n.value)
+        return buf[:n.value]
 
     def query_window(self, k_prime, mode=1):
         """Reports of the window of k_prime < k slices ending at the last closed slice."""

@@ -102,6 +102,10 @@ struct Ctx {
   // last slice
   uint32_t last_n = 0, last_above = 0;
   bool have_reports = false;
+  // asse_end_slice_async: one closed slice whose results are still on the way
+  bool pending = false;
+  uint32_t pend_mode = 0, pend_K = 0;
+  cudaEvent_t ev_collect = nullptr;
   // peers
   bool peers = false;
   uint32_t sync_mode = 0, epoch = 0;
@@ -125,6 +129,13 @@ struct Ctx {
   } while (0)
 
 #define LAUNCHED(c_) ((c_)->stats.kernel_launches++)
+
+#define NOT_PENDING(c_)                                                                   \
+  do {                                                                                    \
+    if ((c_)->pending) { (c_)->err = "results of an asynchronous end_slice pending: call " \
+                                     "asse_end_slice_wait first"; return ASSE_E_STATE; }   \
+  } while (0)
+
 
 static uint64_t splitmix_next(uint64_t* st) {  // A14
   uint64_t z = (*st += 0x9E3779B97F4A7C15ULL);
@@ -783,6 +794,7 @@ uint64_t asse_exchange_bytes(const void* ctx) {
 asse_status asse_merge(void* ctx) {
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
+  NOT_PENDING(c);
   if (!c->peers) { c->err = "asse_merge without attached peers"; return ASSE_E_PEER; }
   CK(cudaSetDevice(c->device));
   return do_merge(c);
@@ -927,20 +939,33 @@ static constexpr int kEndSliceKernels = 3;   // fold, restore (+NAT), sort
 // Copies the counters and a K-report prefix, synchronises once, runs the device-wide
 // sort when |CSIP| exceeds the block sort, records statistics, advances the clock
 // when closing a slice (a9), and hands the reports to the caller.
-static asse_status collect(Ctx* c, uint32_t mode, uint32_t K, asse_report* h_out, uint32_t cap,
-                           uint32_t* n_out, bool advance) {
-  const asse_config& p = c->cfg;
+// results: counters plus a prefix of the requested report array, copied behind the slice's
+// kernels; ev_collect marks their arrival. With advance the slice counts as closed here
+// (a9: t+1, C0; preserveAT for t+1 was applied by k_fold, Alg. 2), so the next slice's
+// scans may be issued before the results are read.
+static asse_status collect_enqueue(Ctx* c, uint32_t mode, uint32_t K, bool advance) {
   cudaStream_t s = c->stream;
-  // results: counters plus a prefix of the requested report array, one synchronisation
   CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(c->h_rep, mode ? c->rep_sorted : c->rep_above, (size_t)K * sizeof(ReportDev),
                      cudaMemcpyDeviceToHost, s));
   if (c->timing && advance) CK(cudaEventRecord(c->ev[9], s));
+  if (!c->ev_collect) CK(cudaEventCreateWithFlags(&c->ev_collect, cudaEventDisableTiming));
+  CK(cudaEventRecord(c->ev_collect, s));
   if (advance) {
     c->stats.kernel_launches += kEndSliceKernels + (c->peers && c->sync_mode == 0 ? 3 : 0);
     c->stats.fold_launches++;
+    c->t += 1;
+    c->C0 = (uint32_t)(c->t % c->two_k);
+    c->stats.slices_closed++;
   }
-  CK(cudaStreamSynchronize(s));
+  return ASSE_OK;
+}
+
+static asse_status collect_finish(Ctx* c, uint32_t mode, uint32_t K, asse_report* h_out, uint32_t cap,
+                                  uint32_t* n_out, bool advance) {
+  const asse_config& p = c->cfg;
+  cudaStream_t s = c->stream;
+  CK(cudaEventSynchronize(c->ev_collect));
   const uint32_t n_cand_raw = c->h_counters[c->shard ? 6 : 0];
   const bool overflow = c->h_counters[1] != 0 || n_cand_raw > p.max_candidates;
   const uint32_t n_cand = overflow ? 0 : n_cand_raw;
@@ -982,12 +1007,7 @@ static asse_status collect(Ctx* c, uint32_t mode, uint32_t K, asse_report* h_out
     asse_status hs = harvest_scan_timing(c);
     if (hs != ASSE_OK) return hs;
   }
-  if (advance) {
-    // a9: advance; preserveAT for t+1 already applied by k_fold (Alg. 2)
-    c->t += 1;
-    c->C0 = (uint32_t)(c->t % c->two_k);
-    c->stats.slices_closed++;
-  }
+
   if (overflow) {
     c->last_n = c->last_above = 0;
     c->err = "CSIP exceeded max_candidates (or the restore join workspace)";
@@ -1004,11 +1024,17 @@ static asse_status collect(Ctx* c, uint32_t mode, uint32_t K, asse_report* h_out
   return copy_reports(c, h_out, cap, n_out, mode);
 }
 
-
+static asse_status collect(Ctx* c, uint32_t mode, uint32_t K, asse_report* h_out, uint32_t cap,
+                           uint32_t* n_out, bool advance) {
+  asse_status st = collect_enqueue(c, mode, K, advance);
+  if (st != ASSE_OK) return st;
+  return collect_finish(c, mode, K, h_out, cap, n_out, advance);
+}
 
 asse_status asse_end_slice_begin(void* ctx) {
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
+  NOT_PENDING(c);
   if (!c->shard || !c->peers || c->sync_mode != 1) {
     c->err = "asse_end_slice_begin is for frame_shard contexts with sync_mode 1";
     return ASSE_E_STATE;
@@ -1030,10 +1056,7 @@ asse_status asse_end_slice_begin(void* ctx) {
   return ASSE_OK;
 }
 
-asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
-  if (!ctx) return ASSE_E_PARAM;
-  Ctx* c = static_cast<Ctx*>(ctx);
-  if (n_out) *n_out = 0;
+static asse_status end_slice_enqueue(Ctx* c, uint32_t mode, uint32_t* K_out) {
   if (mode > 1) { c->err = "mode must be 0 or 1"; return ASSE_E_PARAM; }
   if (closed_all(c)) { c->err = "all n_slices closed"; return ASSE_E_STATE; }
   if (c->cfg.world > 1 && !c->peers) { c->err = "world > 1 requires asse_attach_peers"; return ASSE_E_PEER; }
@@ -1064,7 +1087,42 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
     }
     CK(cudaGraphLaunch(ge, s));
   }
-  return collect(c, mode, K, h_out, cap, n_out, true);
+  *K_out = K;
+  return collect_enqueue(c, mode, K, true);
+}
+
+asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (n_out) *n_out = 0;
+  NOT_PENDING(c);
+  uint32_t K = 0;
+  asse_status st = end_slice_enqueue(c, mode, &K);
+  if (st != ASSE_OK) return st;
+  return collect_finish(c, mode, K, h_out, cap, n_out, true);
+}
+
+asse_status asse_end_slice_async(void* ctx, uint32_t mode) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  NOT_PENDING(c);
+  uint32_t K = 0;
+  asse_status st = end_slice_enqueue(c, mode, &K);
+  if (st != ASSE_OK) return st;
+  c->pending = true;
+  c->pend_mode = mode;
+  c->pend_K = K;
+  return ASSE_OK;
+}
+
+asse_status asse_end_slice_wait(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (n_out) *n_out = 0;
+  if (!c->pending) { c->err = "no asynchronous end_slice pending"; return ASSE_E_STATE; }
+  c->pending = false;
+  CK(cudaSetDevice(c->device));
+  return collect_finish(c, c->pend_mode, c->pend_K, h_out, cap, n_out, true);
 }
 
 // Window query for k' < k on the closed pool (checkAT for any
@@ -1075,6 +1133,7 @@ asse_status asse_query_window(void* ctx, uint32_t k_prime, asse_report* h_out, u
                               uint32_t* n_out, uint32_t mode) {
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
+  NOT_PENDING(c);
   if (n_out) *n_out = 0;
   if (mode > 1) { c->err = "mode must be 0 or 1"; return ASSE_E_PARAM; }
   if (k_prime < 1 || k_prime >= c->cfg.k) { c->err = "query window needs 1 <= k' < k"; return ASSE_E_PARAM; }
@@ -1100,6 +1159,7 @@ asse_status asse_query_window(void* ctx, uint32_t k_prime, asse_report* h_out, u
 asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
+  NOT_PENDING(c);
   if (!c->have_reports) { c->err = "no closed slice"; return ASSE_E_STATE; }
   if (mode > 1) return ASSE_E_PARAM;
   CK(cudaSetDevice(c->device));
@@ -1122,6 +1182,7 @@ struct CkptHeader {
 asse_status asse_save_state(void* ctx, const char* path) {
   if (!ctx || !path) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
+  NOT_PENDING(c);
   CK(cudaSetDevice(c->device));
   CkptHeader h{};
   memcpy(h.magic, "ASSECKPT", 8);
@@ -1143,6 +1204,7 @@ asse_status asse_save_state(void* ctx, const char* path) {
 asse_status asse_load_state(void* ctx, const char* path) {
   if (!ctx || !path) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
+  NOT_PENDING(c);
   CK(cudaSetDevice(c->device));
   FILE* f = fopen(path, "rb");
   if (!f) { c->err = std::string("cannot open ") + path; return ASSE_E_PARAM; }
@@ -1180,6 +1242,7 @@ uint64_t asse_pool_size(const void* ctx) {
 asse_status asse_export_pool(void* ctx, uint16_t* h_out, uint64_t n) {
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
+  NOT_PENDING(c);
   if (!h_out || n != c->n_at) { c->err = "export_pool: n must equal asse_pool_size()"; return ASSE_E_PARAM; }
   CK(cudaSetDevice(c->device));
   if (c->cb == 2) {

@@ -94,3 +94,35 @@ def test_boundary_spanner_sliding_vs_discrete(cuda_device):
             d, ptr = to_device(pk)
             ds.scan_slice(ptr, len(pk))
         assert H not in set(ds.end_slice(0)["ip"].tolist())
+
+
+@pytest.mark.parametrize("name,N,T,variant", [("C1", 200_000, 6, 0), ("C3", 1_500_000, 4, 2)])
+def test_async_end_slice_pipeline(cuda_device, name, N, T, variant):
+    """asse_end_slice_async + asse_end_slice_wait with the next slice's scan issued in
+    between (the bench's pipelined step) gives every slice's reports and the final pool
+    of the oracle run; other calls are refused while results are pending."""
+    p = dict(PRESETS[name])
+    dev, ora = asse.Asse(**p), O.Oracle(**p)
+    dev.set_scan_variant(variant)
+    g = Generator(name, N=N)
+    live, expect = [], None
+    for t in range(T):
+        pk = g.slice(t)
+        d, ptr = to_device(pk)
+        live = (live + [d])[-2:]                 # device input must outlive its scan
+        dev.scan_slice(ptr, len(pk))
+        ora.scan(pk)
+        if t:
+            compare_reports(dev.end_slice_wait(), expect, p["theta"], "%s async t=%d" % (name, t - 1))
+        dev.end_slice_async(1)
+        expect = ora.end_slice(1)
+        if t == 1:
+            with pytest.raises(asse.AsseError):
+                dev.pool()
+            with pytest.raises(asse.AsseError):
+                dev.end_slice_async(1)
+    compare_reports(dev.end_slice_wait(), expect, p["theta"], "%s async last" % name)
+    with pytest.raises(asse.AsseError):
+        dev.end_slice_wait()
+    compare_pool(dev.pool(), ora.pool(), "%s async pool" % name)
+    assert dev.clock()[0] == T
