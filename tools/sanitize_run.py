@@ -54,3 +54,20 @@ for t in range(2):
     print("ranks", t, [len(ctx.end_slice(1)) for ctx in ranks], flush=True)
 torch.cuda.synchronize()
 print("sanitize run ok", flush=True)
+
+# binned scan (k_scan_bin) on the C3 geometry: forced variant, ragged + misaligned calls,
+# pipelined end_slice
+p3 = dict(PRESETS["C3"])
+b = asse.Asse(**p3)
+b.set_scan_variant(2)
+g3 = Generator("C3", N=400_001)
+for t in range(3):
+    pk = g3.slice(t)
+    d = dev(pk)
+    b.scan_slice(d.data_ptr() + 8, len(pk) - 1)
+    b.scan_slice(d.data_ptr(), 3)
+    if t:
+        print("C3 bin", t - 1, len(b.end_slice_wait()), flush=True)
+    b.end_slice_async(1)
+    torch.cuda.synchronize()
+print("C3 bin last", len(b.end_slice_wait()), flush=True)
