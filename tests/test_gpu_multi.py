@@ -23,8 +23,22 @@ pytestmark = pytest.mark.gpu
 def test_virtual_ranks_merge_equals_single(cuda_device, name, D, N, T, shard):
     """shard 0: replicated pools (option R); shard 1: rank d keeps frames
     [d F/D, (d+1) F/D) (option S) and the reports are gathered from every rank."""
+    _run_virtual_ranks(name, D, N, T, shard, 0)
+
+
+@pytest.mark.parametrize("shard", [0, 1])
+@pytest.mark.parametrize("name,D,N,T", [("C3", 2, 3_000_000, 2), ("C4", 4, 2_400_000, 2)])
+def test_virtual_ranks_binned_scan(cuda_device, name, D, N, T, shard):
+    """The same with every rank's scan forced onto k_scan_bin (its write-back lands in the
+    rank's peer-visible touch bitmap)."""
+    _run_virtual_ranks(name, D, N, T, shard, 2)
+
+
+def _run_virtual_ranks(name, D, N, T, shard, variant):
     p = dict(PRESETS[name])
     ranks = [asse.Asse(**dict(p, world=D, rank=d, frame_shard=shard)) for d in range(D)]
+    for ctx in ranks:
+        ctx.set_scan_variant(variant)
     bufs = attach_local_peers(ranks)
     single = asse.Asse(**p)
     ora = O.Oracle(**p)
