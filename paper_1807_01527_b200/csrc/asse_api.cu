@@ -317,6 +317,11 @@ static asse_status launch_scan_bin(Ctx* c, const uint2* pk, uint64_t n, const Sc
   cudaError_t e;
   if (c->cfg.mangle) e = c->cb == 1 ? coop_launch_bin_rr<1, true>(c, pk, n, bp, st) : coop_launch_bin_rr<2, true>(c, pk, n, bp, st);
   else e = c->cb == 1 ? coop_launch_bin_rr<1, false>(c, pk, n, bp, st) : coop_launch_bin_rr<2, false>(c, pk, n, bp, st);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    // fewer SMs than at init (e.g. shared with another context): k_scan does this call
+    cudaGetLastError();
+    return ASSE_E_CAPACITY;
+  }
   CK(e);
   CK(cudaEventRecord(g_bin_last[dev], st));
   if (bp.prof) {   // tools: ASSE_SCAN_PROF=1 prints per-phase cycles of the binned scan (syncs)
@@ -366,9 +371,9 @@ static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cuda
   const uint2* pk = reinterpret_cast<const uint2*>(d_pairs);
   const bool use_bin = c->bin_ok && (c->scan_variant == 2 ||
                                      (c->scan_variant == 0 && tiles * kScanTileBytes >= (uint64_t)c->bin_G * kBinMinTilesPerCta * c->bin_tile));
-  if (use_bin) {
-    asse_status s = launch_scan_bin(c, pk, n, p, st);
-    if (s != ASSE_OK) return s;
+  asse_status bs = use_bin ? launch_scan_bin(c, pk, n, p, st) : ASSE_E_CAPACITY;
+  if (use_bin && bs != ASSE_OK && bs != ASSE_E_CAPACITY) return bs;
+  if (use_bin && bs == ASSE_OK) {
   } else if (c->cfg.mangle) {
     if (c->cb == 1) k_scan<1, true><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
     else k_scan<2, true><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
