@@ -13,6 +13,8 @@ KBIN_CAP, KBIN_QG, KBIN_QCAP = 64, 4, 4096     # asse_scan_bin.cuh
 def bin_geometry(p, sms, rr=1):
     F, E, wpa = 1 << p["u"], 1 << p["c"], p["g"] // 32
     row_words = F * E * wpa
+    if (p["r"] * row_words) // sms <= 16384:
+        rr = 0
     if ((p["r"] - rr) * row_words) // sms <= 256:
         rr = 0
     words = (p["r"] - rr) * row_words
