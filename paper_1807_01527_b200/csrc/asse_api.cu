@@ -87,6 +87,7 @@ struct Ctx {
   uint32_t* h_counters = nullptr;
   ReportDev* h_rep = nullptr;       // fixed prefix buffer (a CUDA-graph copy target)
   uint64_t h_rep_cap = 0;
+  uint32_t sort_bound = 0;          // > 0: the end_slice graph sorts this many slots on the device
   ReportDev* h_big = nullptr;       // larger report copies
   uint64_t h_big_cap = 0;
   // host-buffer scan staging (P:428 double buffering)
@@ -815,7 +816,6 @@ static asse_status copy_reports(Ctx* c, asse_report* h_out, uint32_t cap, uint32
   if (n > cap) return ASSE_E_CAPACITY;
   if (c->h_rep_cap < n) {
     if (c->h_rep) cudaFreeHost(c->h_rep);
-  if (c->h_big) cudaFreeHost(c->h_big);
     c->h_rep = nullptr;
     c->h_rep_cap = std::max<uint64_t>(n, 4096);
     CK(cudaMallocHost(&c->h_rep, c->h_rep_cap * sizeof(ReportDev)));
@@ -859,10 +859,32 @@ static asse_status enqueue_gather(Ctx* c) {
   return ASSE_OK;
 }
 static asse_status enqueue_sort(Ctx* c) {
+  const uint32_t* n_ptr = c->counters + (c->shard ? 6 : 0);
   CK(launch_pdl(k_sort, dim3(kSortBlocks), dim3(kSortThreads), 0, c->stream, (const ReportDev*)c->rep,
-                c->counters, (const uint32_t*)(c->counters + (c->shard ? 6 : 0)),
-                (uint32_t)c->cfg.max_candidates, c->rep_sorted, c->rep_above));
+                c->counters, n_ptr, (uint32_t)c->cfg.max_candidates, c->rep_sorted, c->rep_above));
+  if (c->sort_bound > kSortCap) {
+    // |CSIP| beyond the block sort was seen: sort a bound of slots on the device (A24, A21)
+    cudaStream_t s = c->stream;
+    const uint32_t B = c->sort_bound, mc = c->cfg.max_candidates;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((B + 255) / 256, (uint64_t)c->sms * 8);
+    k_sort_prep<<<blocks, 256, 0, s>>>(n_ptr, B, mc, c->keys, c->vals, c->counters);
+    CK(cudaGetLastError());
+    cub::DoubleBuffer<uint32_t> dk(c->keys, c->keys_alt), dv(c->vals, c->vals_alt);
+    size_t bytes = c->cub_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, dk, dv, (int)B, 0, 32, s));
+    k_gather_bound<<<blocks, 256, 0, s>>>(c->rep, dv.Current(), n_ptr, B, mc, c->rep_sorted);
+    CK(cudaGetLastError());
+    bytes = c->cub_bytes;
+    CK(cub::DeviceSelect::If(c->cub_tmp, bytes, c->rep_sorted, c->rep_above, c->counters + 4, (int)B,
+                             AboveTheta(), s));
+  }
   return ASSE_OK;
+}
+
+static void drop_graphs(Ctx* c) {
+  for (auto& row : c->graph)
+    for (auto& g : row)
+      if (g) { cudaGraphExecDestroy(g); g = nullptr; }
 }
 static asse_status enqueue_tail(Ctx* c) {
   asse_status st = enqueue_restore(c);
@@ -960,7 +982,8 @@ static asse_status collect_enqueue(Ctx* c, uint32_t mode, uint32_t K, bool advan
   if (!c->ev_collect) CK(cudaEventCreateWithFlags(&c->ev_collect, cudaEventDisableTiming));
   CK(cudaEventRecord(c->ev_collect, s));
   if (advance) {
-    c->stats.kernel_launches += kEndSliceKernels + (c->peers && c->sync_mode == 0 ? 3 : 0);
+    c->stats.kernel_launches += kEndSliceKernels + (c->peers && c->sync_mode == 0 ? 3 : 0) +
+                                (c->sort_bound > kSortCap ? 8 : 0);   // prep, radix passes, gather, select
     c->stats.fold_launches++;
     c->t += 1;
     c->C0 = (uint32_t)(c->t % c->two_k);
@@ -995,6 +1018,11 @@ static asse_status collect_finish(Ctx* c, uint32_t mode, uint32_t K, asse_report
     CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     prefetched = false;
+    // later slices sort on the device inside the end_slice graph (bound with 50 % headroom)
+    uint64_t B = kSortCap * 2ull;
+    while (B < (uint64_t)n_cand + n_cand / 2) B *= 2;
+    c->sort_bound = (uint32_t)std::min<uint64_t>(B, p.max_candidates);
+    drop_graphs(c);
   }
   c->last_n = n_cand;
   c->last_above = n_cand ? c->h_counters[4] : 0;
@@ -1072,7 +1100,17 @@ static asse_status end_slice_enqueue(Ctx* c, uint32_t mode, uint32_t* K_out) {
   const asse_config& p = c->cfg;
   cudaStream_t s = c->stream;
   const bool timing = c->timing;
-  const uint32_t K = (uint32_t)std::min<uint64_t>(c->h_rep_cap, p.max_candidates);
+  // report prefix copied with the counters: enough for the last slice's count + 25 %, so a
+  // stable workload never needs a second copy (and synchronisation)
+  uint64_t want = std::max<uint64_t>(4096, (uint64_t)(mode ? c->last_n : c->last_above) * 5 / 4 + 64);
+  want = std::min<uint64_t>(want, p.max_candidates);
+  if (want > c->h_rep_cap) {
+    if (c->h_rep) CK(cudaFreeHost(c->h_rep));
+    c->h_rep = nullptr;
+    c->h_rep_cap = std::min<uint64_t>(std::max<uint64_t>(want * 2, 4096), p.max_candidates);
+    CK(cudaMallocHost(&c->h_rep, c->h_rep_cap * sizeof(ReportDev)));
+  }
+  const uint32_t K = (uint32_t)std::min<uint64_t>(want, c->h_rep_cap);
   // the per-slice ACT base reaches the kernels through device memory, so the captured
   // graph is identical for every slice (host copies stay outside the graph)
   *c->h_clock = c->C0;

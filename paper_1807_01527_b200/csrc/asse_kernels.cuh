@@ -732,6 +732,31 @@ __global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
   pdl_trigger();
 }
 
+// In-graph device-wide sort for |CSIP| above the block sort (used once a slice needed it):
+// the radix sort runs over a host-chosen bound B >= |CSIP|, so no host round trip is
+// needed. Slots [n, B) get key 0xFFFFFFFF (a real ip of that value sorts first: the sort is
+// stable and real slots come first); counters[5] (set by k_sort when n > kSortCap) is
+// cleared when n <= B, else the host falls back to the exact-n path.
+__global__ void k_sort_prep(const uint32_t* __restrict__ n_ptr, uint32_t bound, uint32_t max_cand,
+                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* counters) {
+  const uint32_t n = min(*n_ptr, max_cand);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n <= bound) counters[5] = 0u;
+  for (uint32_t q = n + blockIdx.x * blockDim.x + threadIdx.x; q < bound; q += gridDim.x * blockDim.x) {
+    keys[q] = 0xFFFFFFFFu;
+    vals[q] = q;
+  }
+}
+// sorted order -> reports; slots >= n become empty reports (flags 0: not selected)
+__global__ void k_gather_bound(const ReportDev* __restrict__ in, const uint32_t* __restrict__ order,
+                               const uint32_t* __restrict__ n_ptr, uint32_t bound, uint32_t max_cand,
+                               ReportDev* __restrict__ out_all) {
+  const uint32_t n = min(*n_ptr, max_cand);
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < bound; q += gridDim.x * blockDim.x) {
+    if (q < n) out_all[q] = in[order[q]];
+    else out_all[q] = ReportDev{0xFFFFFFFFu, 0u, 0.0, 0u, 0u};
+  }
+}
+
 // gather reports in ascending-ip order (A24)
 __global__ void k_gather(const ReportDev* __restrict__ in, const uint32_t* __restrict__ order,
                          uint32_t n, ReportDev* __restrict__ out_all) {
