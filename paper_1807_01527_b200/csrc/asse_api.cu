@@ -562,7 +562,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
       if (!getenv("ASSE_SCAN_RR") && (p.r * row_words) / c->bin_G <= 16384) c->bin_rr = 0;
       if (((p.r - c->bin_rr) * row_words) / c->bin_G <= 256) c->bin_rr = 0;
       const uint64_t words = (p.r - c->bin_rr) * row_words;
-      c->bin_tile = (uint32_t)((4096 / (4 - c->bin_rr)) * 8 / 16 * 16);
+      c->bin_tile = (uint32_t)(((uint32_t)(kBinCap * 64) / (4 - c->bin_rr)) * 8 / 16 * 16);   // kBinCap * 64 binned updates per round
       c->bin_wpo = (uint32_t)(((words + c->bin_G - 1) / c->bin_G + 3) & ~3ull);
       c->bin_inv = (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, ((1ull << 40) + c->bin_wpo - 1) / c->bin_wpo);
       c->bin_smem = bin_smem_bytes(c->bin_G, c->bin_wpo, c->bin_tile);

@@ -34,9 +34,9 @@ constexpr int kBinTmaWarp = kBinConsWarp0 + kBinConsWarps; // packet tiles -> sh
 constexpr int kBinSigWarp = kBinTmaWarp + 1;               // publishes rounds (release fence off the
                                                            // binning warps' path)
 constexpr int kBinThreads = 32 * (kBinSigWarp + 1);
-constexpr int kBinRing = 4;                                // packet-tile ring stages
-constexpr int kBinCap = 64;                                // staged entries per (owner, round) in a CTA
-constexpr int kBinStride = 68;                             // words between bins: bin o starts at bank
+constexpr int kBinRing = 2;                                // packet-tile ring stages
+constexpr int kBinCap = 88;                                // staged entries per (owner, round) in a CTA
+constexpr int kBinStride = 92;                             // words between bins: bin o starts at bank
                                                            // 4o mod 32, so equal slots of different bins
                                                            // do not collide (16-B aligned)
 constexpr int kBinNB = 4;                                  // queue buffers (rounds) in flight
@@ -348,6 +348,17 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
 #pragma unroll
         for (int k = 0; k < NS; ++k)
           if (4 * hl < c4[k]) dst[k * kDstStep + (((of[k] >> 2) + hl) & (kBinQCap / 4 - 1))] = v[k];
+        // bins longer than 64 entries: 16-B groups 16.. of those owners (rare)
+        if (kBinCap > 64) {
+#pragma unroll
+          for (int k = 0; k < NS; ++k)
+            if (4 * (hl + 16) < c4[k]) {
+              uint4 x;
+              asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "r"(src_s + k * kSrcStep + 256u));
+              dst[k * kDstStep + (((of[k] >> 2) + hl + 16) & (kBinQCap / 4 - 1))] = x;
+            }
+        }
         if (my_o < G) scount[sf * Gp + my_o] = 0;
         __syncwarp();
         if (lane == 0) mbar_arrive(&sigbar[tf % kSig]);   // this warp wrote round tf (release.cta)

@@ -7,7 +7,7 @@ import pytest
 
 from gen import PRESETS
 
-KBIN_CAP, KBIN_QG, KBIN_QCAP = 64, 4, 4096     # asse_scan_bin.cuh
+KBIN_CAP, KBIN_QG, KBIN_QCAP = 88, 4, 4096     # asse_scan_bin.cuh
 
 
 def bin_geometry(p, sms, rr=1):
