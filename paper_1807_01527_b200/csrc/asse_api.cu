@@ -562,7 +562,13 @@ asse_status asse_init(const asse_config* cfg, void** out) {
       if (!getenv("ASSE_SCAN_RR") && (p.r * row_words) / c->bin_G <= 16384) c->bin_rr = 0;
       if (((p.r - c->bin_rr) * row_words) / c->bin_G <= 256) c->bin_rr = 0;
       const uint64_t words = (p.r - c->bin_rr) * row_words;
-      c->bin_tile = (uint32_t)(((uint32_t)(kBinCap * 64) / (4 - c->bin_rr)) * 8 / 16 * 16);   // kBinCap * 64 binned updates per round
+      // packets per CTA per round: a multiple of 1024 (every binning thread handles the same
+      // number of 16-B groups), ~kBinCap * 64 binned updates per round (tools: ASSE_SCAN_TILE)
+      {
+        uint32_t pk = ((uint32_t)(kBinCap * 64) / (4 - c->bin_rr) + 512) / 1024 * 1024;
+        if (const char* e = getenv("ASSE_SCAN_TILE")) pk = ((uint32_t)atoi(e) + 1u) & ~1u;
+        c->bin_tile = std::max<uint32_t>(1024, pk) * 8;
+      }
       c->bin_wpo = (uint32_t)(((words + c->bin_G - 1) / c->bin_G + 3) & ~3ull);
       c->bin_inv = (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, ((1ull << 40) + c->bin_wpo - 1) / c->bin_wpo);
       c->bin_smem = bin_smem_bytes(c->bin_G, c->bin_wpo, c->bin_tile);
