@@ -257,7 +257,7 @@ template <int CB> constexpr uint32_t fold_code_bytes() { return kFoldChunksPerTi
 template <int CB> constexpr uint32_t fold_stage_bytes() { return fold_code_bytes<CB>() + kFoldChunksPerTile * 64u; }
 // u8 full fold: results are staged in shared memory and written back by a storer warp
 // with bulk (TMA) stores: codes, active words and the zeroed touch words of a tile.
-template <int CB, bool WEIGH> constexpr bool fold_tma_out() { return CB == 1 && !WEIGH; }
+template <int CB, bool WEIGH> constexpr bool fold_tma_out() { return !WEIGH; }
 constexpr int kFoldOutStages = 2;
 template <int CB, bool WEIGH> constexpr int fold_threads() {
   return 32 * (kFoldConsumerWarps + 1 + (fold_tma_out<CB, WEIGH>() ? 1 : 0));
