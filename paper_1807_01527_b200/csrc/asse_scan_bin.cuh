@@ -4,18 +4,23 @@
 // bitmap and runs at ~0.9 of the measured random-op ceiling (~188 Gop/s, 1.56
 // SM-cycles per update, tools/l2bench.cu). A random shared-memory atomic costs 0.18
 // SM-cycles and a coalesced 16-byte global access a small fraction of that
-// (tools/smembench.cu, profiles/). The bitmaps of the BASELINE geometries
-// (16 MiB at C3-C5) fit in the sum of the SMs' shared memories, so:
+// (tools/smembench.cu, profiles/r01_smembench.txt). The bitmaps of the BASELINE
+// geometries (16 MiB at C3-C5) fit in the sum of the SMs' shared memories, so
+// (DESIGN.md §5.4):
 //
 //  * one persistent CTA per SM (cooperative launch: all CTAs co-resident); CTA o OWNS
-//    touch words [o*wpo, (o+1)*wpo) and keeps them in shared memory for the whole call;
-//  * round t: every CTA takes one 16 KB packet tile (2048 packets, TMA bulk copy into a
-//    2-stage ring), computes the r SetAT targets of each packet exactly as k_scan does,
-//    and bins them by owner in shared memory (one shared atomic for the slot + a store);
-//  * it flushes bin o to its fixed slot [t mod NB][o][me] of a global queue (coalesced
-//    16-byte stores, L2-resident) and publishes the round with a release counter;
-//  * consumer warps of CTA o wait for round t to be published by every CTA and apply
-//    the entries addressed to it with shared-memory atomicOr;
+//    words [o*wpo, (o+1)*wpo) of the binned rows and keeps them in shared memory for the
+//    whole call; rows y < RR keep k_scan's RED route into L2 (RR = 1 at C3-C5);
+//  * round t: every CTA takes one packet tile (2048 packets at RR = 1, TMA bulk copy into
+//    a 2-stage ring); 16 binning warps compute the SetAT targets exactly as k_scan does and
+//    bin the binned rows' updates by owner in a double-buffered staging area (one shared
+//    atomic for the slot + a predicated store);
+//  * while round t is binned, round t-1's bins are padded to 16 B, their ranges reserved in
+//    the owner rings [t mod NB][o][producer group] with one global atomicAdd each (issued
+//    before the binning, so its latency hides) and copied with 16-byte stores; a signal
+//    warp publishes the round (release fence + counter);
+//  * eight draining warps (two groups, round parity) wait for a round to be published by
+//    every CTA and apply their owner's entries with shared-memory atomicOr;
 //  * at the end every CTA ORs its owned words into the global touch bitmap.
 //
 // A bin that overflows its CAP entries in one round falls back to a direct RED.OR of
@@ -27,7 +32,7 @@
 
 namespace asse {
 
-constexpr int kBinBinWarps = 16;                           // binning + flushing warps
+constexpr int kBinBinWarps = 16;                           // binning + shipping warps
 constexpr int kBinConsWarps = 8;                           // queue-draining warps, two groups (round parity)
 constexpr int kBinConsWarp0 = kBinBinWarps;
 constexpr int kBinTmaWarp = kBinConsWarp0 + kBinConsWarps; // packet tiles -> shared ring (TMA)
@@ -69,11 +74,6 @@ __host__ __device__ constexpr size_t bin_smem_bytes(uint32_t G, uint32_t wpo, ui
          16 + (size_t)wpo * 4;
 }
 
-__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -105,25 +105,11 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, u
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(threads) : "memory");
 }
-__device__ __forceinline__ void named_arrive(int id, int threads) {
-  asm volatile("bar.arrive %0, %1;" :: "r"(id), "r"(threads) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
 
 // shared-space (32-bit address) accessors: no generic-to-shared conversion per access
 __device__ __forceinline__ uint32_t atoms_inc(uint32_t addr) {
   uint32_t old;
   asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(addr) : "memory");
-  return old;
-}
-// bin slot = old value of the owner's counter; 0 (no access) when !pred
-__device__ __forceinline__ uint32_t atoms_inc_if(bool pred, uint32_t addr) {
-  uint32_t old;
-  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n mov.u32 %0, 0;\n"
-               " @p atom.shared.add.u32 %0, [%2], 1;\n}"
-               : "=r"(old) : "r"((uint32_t)pred), "r"(addr) : "memory");
   return old;
 }
 __device__ __forceinline__ void sts_if(bool pred, uint32_t addr, uint32_t v) {
