@@ -95,3 +95,27 @@ def test_variant_validation(cuda_device):
     with pytest.raises(asse.AsseError):
         big.set_scan_variant(2)
     big.set_scan_variant(0)
+
+
+def test_binned_on_caller_stream_and_host_ingest(cuda_device):
+    """k_scan_bin launched on a caller stream (asse_scan_slice's stream argument) and fed
+    by the host double-buffered ingest (asse_scan_slice_host, 8 Mi-packet chunks)."""
+    import torch
+    dev, ora, p = _pair("C3", 2)
+    g = Generator("C3", N=9_000_001)
+    side = torch.cuda.Stream()
+    pk = g.slice(0)
+    with torch.cuda.stream(side):
+        d = torch.from_numpy(pk.view(np.int32).reshape(-1)).to("cuda", non_blocking=False)
+    dev.scan_slice(d, stream=side.cuda_stream)
+    ora.scan(pk)
+    rd, ro = dev.end_slice(1), ora.end_slice(1)
+    assert (rd["ip"] == ro["ip"]).all() and (rd["nat"] == ro["nat"]).all()
+    assert (dev.pool() == ora.pool()).all()
+    pk = g.slice(1)
+    dev.scan_slice_host(np.ascontiguousarray(pk))
+    ora.scan(pk)
+    rd, ro = dev.end_slice(1), ora.end_slice(1)
+    assert (rd["ip"] == ro["ip"]).all() and (rd["nat"] == ro["nat"]).all()
+    assert (dev.pool() == ora.pool()).all()
+    assert dev.stats()["scan_bin_launches"] >= 3
