@@ -203,8 +203,9 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=20_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--scan-variant", type=int, default=0, choices=[0, 1, 2],
-                    help="0 auto, 1 k_scan (direct RED.OR into L2), 2 k_scan_bin (shared-memory bins)")
+    ap.add_argument("--scan-variant", type=int, default=0, choices=[0, 1, 2, 3],
+                    help="0 auto, 1 k_scan (direct RED.OR into L2), 2 k_scan_bin (shared-memory bins), "
+                         "3 k_scan_own (packet-owned shared-memory slices)")
     ap.add_argument("--replicated", action="store_true",
                     help="N>1: keep the whole pool on every GPU (option R) instead of frame sharding (S)")
     args = ap.parse_args()
@@ -313,7 +314,8 @@ def main():
     fold_launch_ms = (sb["fold_ms_total"] - sa["fold_ms_total"]) / max(1, sb["fold_launches"] - sa["fold_launches"])
     cb = st1["code_bytes"]
     binned = sb["scan_bin_launches"] > sa["scan_bin_launches"]
-    scan_kernel = "k_scan_bin" if binned else "k_scan"
+    owned = sb["scan_own_launches"] > sa["scan_own_launches"]
+    scan_kernel = "k_scan_own" if owned else "k_scan_bin" if binned else "k_scan"
     peak, peak_src = load_peaks()
     scan_bytes = n_local * (8 + p["r"] * cb)          # 8 B read + r codes written
     scan_gbs = scan_bytes / (scan_launch_ms / 1e3) / 1e9
@@ -407,12 +409,14 @@ def main():
                                "l2_random_red_ceiling": (load_l2_peak() or float("nan")) / 1e9,
                                "frac_of_l2_random_red_ceiling": (p["r"] * n_local / (scan_launch_ms / 1e3))
                                / load_l2_peak() if load_l2_peak() else None,
-                               "rows_via_red": st1["scan_rows_red"] if binned else p["r"],
+                               "rows_via_red": 0 if owned else st1["scan_rows_red"] if binned else p["r"],
                                "peak_source": "profiles/l2_random_peak.json (tools/l2bench.cu, measured)",
                                "note": "k_scan: r red.global.or.b32 per packet, bound by the L2 random-op "
                                        "ceiling; k_scan_bin: rows below rows_via_red take that route, the "
                                        "others are binned through shared memory and owner queues, which "
-                                       "lifts the SetAT rate above the ceiling"},
+                                       "lifts the SetAT rate above the ceiling; k_scan_own: each packet "
+                                       "travels once to the CTA owning (frame, word group of BH(bip)), which "
+                                       "applies its r SetATs in shared memory"},
             "kernels": {"k_fold": {"avg_launch_ms": fold_launch_ms, "algorithmic_bytes": fold_bytes,
                                    "achieved_gbs": fold_gbs, "frac": fold_gbs / peak}},
             "cpu_baseline": cpu,

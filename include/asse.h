@@ -86,6 +86,8 @@ typedef struct {
   uint32_t scan_bin_launches;    /* cumulative launches of the binned scan (k_scan_bin) */
   uint32_t scan_rows_red;        /* k_scan_bin: rows whose SetATs take the direct RED route */
   uint32_t scan_bin_ok;          /* 1 if k_scan_bin is available for this geometry/device */
+  uint32_t scan_own_launches;    /* cumulative launches of the packet-owned scan (k_scan_own) */
+  uint32_t scan_own_ok;          /* 1 if k_scan_own is available for this geometry/device */
 } asse_stats;
 
 /* Validate a configuration (completeness/redundancy P:315-324, A10; the device

@@ -5,7 +5,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libasse.so")
-SRCS = [os.path.join(PKG, "csrc", f) for f in ("asse_api.cu", "asse_kernels.cuh", "asse_scan_bin.cuh", "asse_tma.cuh")] + [
+SRCS = [os.path.join(PKG, "csrc", f) for f in ("asse_api.cu", "asse_kernels.cuh", "asse_scan_bin.cuh", "asse_scan_own.cuh", "asse_tma.cuh")] + [
     os.path.join(ROOT, "include", "asse.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

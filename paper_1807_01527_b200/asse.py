@@ -57,7 +57,8 @@ class Stats(ctypes.Structure):
                 ("last_n_super", ctypes.c_uint32), ("last_n_candidates", ctypes.c_uint32),
                 ("last_n_above", ctypes.c_uint32), ("w_theta", ctypes.c_uint32),
                 ("code_bytes", ctypes.c_uint32), ("scan_bin_launches", ctypes.c_uint32),
-                ("scan_rows_red", ctypes.c_uint32), ("scan_bin_ok", ctypes.c_uint32)]
+                ("scan_rows_red", ctypes.c_uint32), ("scan_bin_ok", ctypes.c_uint32),
+                ("scan_own_launches", ctypes.c_uint32), ("scan_own_ok", ctypes.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}

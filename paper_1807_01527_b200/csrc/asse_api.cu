@@ -17,6 +17,7 @@
 #include "asse.h"
 #include "asse_kernels.cuh"
 #include "asse_scan_bin.cuh"
+#include "asse_scan_own.cuh"
 
 using namespace asse;
 
@@ -55,6 +56,12 @@ struct Ctx {
   size_t bin_smem = 0;
   uint32_t* bin_queue = nullptr;      // [NB][G][QCAP]
   uint32_t* bin_sync = nullptr;       // [2 NB]
+  // packet-owned scan (asse_scan_own.cuh): owner = (frame, word group of the AT position)
+  bool own_ok = false;
+  uint32_t own_O = 0, own_lg_ngrp = 0, own_lg_wg = 0, own_tile = 0;
+  size_t own_smem = 0;
+  uint2* own_queue = nullptr;         // [NB][O][QG][QCAP]
+  uint32_t* own_sync = nullptr;
   cudaStream_t stream = nullptr, copy_stream = nullptr;
   void* pool = nullptr;
   uint32_t* touch_own = nullptr;
@@ -190,7 +197,7 @@ static void free_all(Ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* dev[] = {c->pool, c->touch_own, c->active, c->scratch, c->sa_list, c->ws, c->cand, c->rep, c->rep_sorted, c->rep_above, c->keys,
                  c->keys_alt, c->vals, c->vals_alt, c->cub_tmp, c->export_buf, c->stage[0],
-                 c->stage[1], c->bin_queue, c->bin_sync};
+                 c->stage[1], c->bin_queue, c->bin_sync, c->own_queue, c->own_sync};
   for (void* p : dev) if (p) cudaFree(p);
   if (c->h_counters) cudaFreeHost(c->h_counters);
   if (c->h_clock) cudaFreeHost(c->h_clock);
@@ -349,6 +356,74 @@ static asse_status launch_scan_bin(Ctx* c, const uint2* pk, uint64_t n, const Sc
   return ASSE_OK;
 }
 
+template <int CB, bool MP>
+static cudaError_t coop_launch_own(Ctx* c, const uint2* pk, uint64_t n, const OwnScanParams& op, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(c->bin_G);
+  cfg.blockDim = dim3(kOwnThreads);
+  cfg.dynamicSmemBytes = c->own_smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_scan_own<CB, MP>, pk, n, op);
+}
+
+static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const ScanParams& sp, cudaStream_t st) {
+  const uint32_t G = c->bin_G, O = c->own_O;
+  const size_t sync_words = (2 * kBinNB + (size_t)kBinNB * O * kBinQG) * kBinPad;
+  if (!c->own_queue) {
+    CK(cudaMalloc(&c->own_queue, (size_t)kBinNB * O * kBinQG * kOwnQCap * sizeof(uint2)));
+    CK(cudaMalloc(&c->own_sync, sync_words * 4));
+  }
+  const int dev = c->device & 63;
+  if (!g_bin_last[dev]) CK(cudaEventCreateWithFlags(&g_bin_last[dev], cudaEventDisableTiming));
+  CK(cudaStreamWaitEvent(st, g_bin_last[dev], 0));
+  OwnScanParams op{};
+  op.sp = sp;
+  op.queue = c->own_queue;
+  op.qcnt = c->own_sync + 2 * kBinNB * kBinPad;
+  op.sync = c->own_sync;
+  op.O = O;
+  op.lg_ngrp = c->own_lg_ngrp;
+  op.lg_wg = c->own_lg_wg;
+  op.tile_bytes = c->own_tile;
+  static const bool prof = getenv("ASSE_SCAN_PROF") != nullptr;
+  if (prof) {
+    static unsigned long long* dprof = nullptr;
+    if (!dprof) CK(cudaMalloc(&dprof, 16 * 1024 * 8));
+    op.prof = dprof;
+  }
+  CK(cudaMemsetAsync(c->own_sync, 0, sync_words * 4, st));
+  cudaError_t e;
+  if (c->cfg.mangle) e = c->cb == 1 ? coop_launch_own<1, true>(c, pk, n, op, st) : coop_launch_own<2, true>(c, pk, n, op, st);
+  else e = c->cb == 1 ? coop_launch_own<1, false>(c, pk, n, op, st) : coop_launch_own<2, false>(c, pk, n, op, st);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    cudaGetLastError();
+    return ASSE_E_CAPACITY;
+  }
+  CK(e);
+  CK(cudaEventRecord(g_bin_last[dev], st));
+  if (op.prof) {
+    std::vector<unsigned long long> h((size_t)G * 16);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(h.data(), op.prof, h.size() * 8, cudaMemcpyDeviceToHost));
+    const char* nm[13] = {"b_bin", "b_wait_reserve", "b_copy", "-", "-", "-",
+                          "-", "-", "-", "c0_wait", "c0_drain", "c1_wait", "c1_drain"};
+    fprintf(stderr, "k_scan_own n=%llu G=%u O=%u:", (unsigned long long)n, G, O);
+    for (int q = 0; q < 13; ++q) {
+      double sum = 0, mx = 0;
+      for (uint32_t b = 0; b < G; ++b) { sum += (double)h[b * 16 + q]; mx = std::max(mx, (double)h[b * 16 + q]); }
+      fprintf(stderr, " %s %.0f/%.0f;", nm[q], sum / G, mx);
+    }
+    fprintf(stderr, "\n");
+  }
+  c->stats.scan_own_launches++;
+  return ASSE_OK;
+}
+
 static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cudaStream_t st) {
   if (n == 0) return ASSE_OK;
   ScanParams p{};
@@ -376,11 +451,13 @@ static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cuda
     CK(cudaEventRecord(e0, st));
   }
   const uint2* pk = reinterpret_cast<const uint2*>(d_pairs);
-  const bool use_bin = c->bin_ok && (c->scan_variant == 2 ||
+  const bool use_own = c->own_ok && (c->scan_variant == 3 ||
+                                     (c->scan_variant == 0 && tiles * kScanTileBytes >= (uint64_t)c->bin_G * kOwnMinTilesPerCta * c->own_tile));
+  const bool use_bin = !use_own && c->bin_ok && (c->scan_variant == 2 ||
                                      (c->scan_variant == 0 && tiles * kScanTileBytes >= (uint64_t)c->bin_G * kBinMinTilesPerCta * c->bin_tile));
-  asse_status bs = use_bin ? launch_scan_bin(c, pk, n, p, st) : ASSE_E_CAPACITY;
-  if (use_bin && bs != ASSE_OK && bs != ASSE_E_CAPACITY) return bs;
-  if (use_bin && bs == ASSE_OK) {
+  asse_status bs = use_own ? launch_scan_own(c, pk, n, p, st) : use_bin ? launch_scan_bin(c, pk, n, p, st) : ASSE_E_CAPACITY;
+  if ((use_own || use_bin) && bs != ASSE_OK && bs != ASSE_E_CAPACITY) return bs;
+  if ((use_own || use_bin) && bs == ASSE_OK) {
   } else if (c->cfg.mangle) {
     if (c->cb == 1) k_scan<1, true><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
     else k_scan<2, true><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
@@ -593,6 +670,37 @@ asse_status asse_init(const asse_config* cfg, void** out) {
       }
       c->stats.scan_rows_red = c->bin_rr;
       c->stats.scan_bin_ok = c->bin_ok ? 1u : 0u;
+      // packet-owned scan: O = F * NGRP owners (NGRP word groups per ATV, a power of two
+      // dividing g/32, F * NGRP <= SMs), slice = r x 2^c ATVs x WG words in shared memory
+      {
+        const uint32_t F = 1u << p.u;
+        uint32_t lg_wpa = 0;
+        while ((1u << lg_wpa) < c->wpa) ++lg_wpa;
+        uint32_t lg_ngrp = 0;
+        while (lg_ngrp < lg_wpa && (F << (lg_ngrp + 1)) <= (uint32_t)c->sms) ++lg_ngrp;
+        c->own_lg_ngrp = lg_ngrp;
+        c->own_lg_wg = lg_wpa - lg_ngrp;
+        c->own_O = F << lg_ngrp;
+        // ~16 entries per bin per round on average (CAP = 30): 2048 packets at O = 128
+        c->own_tile = std::min<uint32_t>(2048u, std::max<uint32_t>(1024u, c->own_O * 16u) / 1024u * 1024u) * 8u;
+        if (const char* e = getenv("ASSE_SCAN_TILE")) c->own_tile = ((uint32_t)atoi(e) + 255u) / 256u * 256u * 8u;
+        const uint64_t slice_words = (uint64_t)p.r << (p.c + c->own_lg_wg);
+        c->own_smem = own_smem_bytes(c->own_O, (uint32_t)std::min<uint64_t>(slice_words, 1u << 30), c->own_tile);
+        c->own_ok = coop && p.r == 4 && (1u << lg_wpa) == c->wpa && c->own_O <= (uint32_t)c->sms &&
+                    c->own_O <= kOwnMaxOwners && c->own_O >= 2 &&
+                    (uint64_t)((c->sms + kBinQG - 1) / kBinQG) * kOwnCap <= kOwnQCap &&
+                    slice_words <= (1u << 20) && c->own_smem + 2048 <= (size_t)optin &&
+                    !getenv("ASSE_SCAN_NO_OWN");
+        if (c->own_ok) {
+          void* fns[4] = {(void*)k_scan_own<1, false>, (void*)k_scan_own<2, false>, (void*)k_scan_own<1, true>,
+                          (void*)k_scan_own<2, true>};
+          for (void* f : fns) CKI(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->own_smem));
+          int oocc = 0;
+          CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oocc, k_scan_own<1, false>, kOwnThreads, c->own_smem));
+          c->own_ok = oocc >= 1;
+        }
+        c->stats.scan_own_ok = c->own_ok ? 1u : 0u;
+      }
     }
     CKI(fold_occupancy(c->cb, c->lpa_log2, c->q_log2, &occ));
     c->fold_grid = std::max(1, occ) * c->sms;
@@ -708,8 +816,12 @@ asse_status asse_set_timing(void* ctx, int enable) {
 asse_status asse_set_scan_variant(void* ctx, int variant) {
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
-  if (variant < 0 || variant > 2) { c->err = "scan variant is 0 (auto), 1 (direct) or 2 (binned)"; return ASSE_E_PARAM; }
+  if (variant < 0 || variant > 3) {
+    c->err = "scan variant is 0 (auto), 1 (direct), 2 (binned) or 3 (packet-owned)";
+    return ASSE_E_PARAM;
+  }
   if (variant == 2 && !c->bin_ok) { c->err = "binned scan unavailable for this geometry/device"; return ASSE_E_PARAM; }
+  if (variant == 3 && !c->own_ok) { c->err = "packet-owned scan unavailable for this geometry/device"; return ASSE_E_PARAM; }
   c->scan_variant = variant;
   return ASSE_OK;
 }

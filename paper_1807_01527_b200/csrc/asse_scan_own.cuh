@@ -1,0 +1,377 @@
+// asse_scan_own.cuh — Alg. 3 with packet-granular ownership of the touch bitmap.
+//
+// k_scan_bin (asse_scan_bin.cuh) bins each of a packet's r SetATs separately: r targets
+// computed by the producer, r slot atomics, r 4-byte queue entries and one row through
+// L2 REDs. Here the unit that travels is the PACKET, not the SetAT. A host's r ATVs share
+// its frame z = f(aip) mod 2^u and all r SetATs of a packet hit the same AT
+// position i = BH(bip) (Alg. 3 computes i once). So the pair (z, word group of i) names a
+// slice of the bitmap that holds all r targets of the packet:
+//
+//   owner o = z * NGRP + (i >> 5) / WG       (NGRP word groups of WG words per ATV)
+//   slice(o) = rows 0..r-1, the 2^c ATVs of frame z, words [grp*WG, (grp+1)*WG) of each
+//
+// At the C3-C5 geometry (F = 16 frames, 2^c = 4096, g = 512: 16 words per ATV) NGRP = 8,
+// WG = 2: 128 owners of 128 KiB each. The producer computes f(aip) and BH(bip), takes one
+// slot in the owner's bin and stores the 8-byte entry {f(aip), i}; the owner derives the r
+// column windows itself and applies the r SetATs with shared-memory atomics.
+// Per packet: 1 slot atomic (k_scan_bin: 3), 8 B through the L2 queues (12 B + a RED), no
+// global RED. CTAs beyond the O owners produce only.
+//
+// Round structure, queues, publication and drain are k_scan_bin's; the
+// touch bits after the call are the same union (SetAT is idempotent within a slice),
+// so the pool after every slice is bit-identical to k_scan's and the oracle's.
+#pragma once
+#include "asse_scan_bin.cuh"
+
+namespace asse {
+
+#ifndef ASSE_OWN_BIN_WARPS
+#define ASSE_OWN_BIN_WARPS 16
+#endif
+#ifndef ASSE_OWN_CONS_WARPS
+#define ASSE_OWN_CONS_WARPS 12
+#endif
+#ifndef ASSE_OWN_CHECK
+#define ASSE_OWN_CHECK 0
+#endif
+#ifndef ASSE_OWN_U
+#define ASSE_OWN_U 1
+#endif
+// warps (measured at C5 on B200, tools/gpu_own_sweep2.sh; the drain is the longer phase):
+// 16 binning + 8 draining warps 0.98 ms, + 10 1.07, + 12 0.94, + 14 0.95 (64 registers)
+constexpr int kOwnBinWarps = ASSE_OWN_BIN_WARPS;           // binning + shipping warps
+constexpr int kOwnConsWarps = ASSE_OWN_CONS_WARPS;         // queue-draining warps, two groups (round parity)
+constexpr int kOwnConsWarp0 = kOwnBinWarps;
+constexpr int kOwnTmaWarp = kOwnConsWarp0 + kOwnConsWarps;
+constexpr int kOwnSigWarp = kOwnTmaWarp + 1;
+constexpr int kOwnThreads = 32 * (kOwnSigWarp + 1);
+constexpr int kOwnRing = 2;                                // packet-tile ring stages
+constexpr int kOwnCap = 30;                                // staged entries per (owner, round) in a CTA
+constexpr int kOwnStride = 30;                             // entries (8 B) between bins: 240 B, 16-B aligned;
+                                                           // bin o starts at bank 28o mod 32
+constexpr uint32_t kOwnQCap = 2048;                        // ring entries per (buffer, owner, group)
+                                                           // >= ceil(G / QG) * kOwnCap
+constexpr uint32_t kOwnMaxOwners = 128;                   // F * NGRP: a power of two <= the SMs
+constexpr uint32_t kOwnMinTilesPerCta = 8;                 // below: k_scan is used
+
+struct OwnScanParams {
+  ScanParams sp;          // hashing parameters and the global touch bitmap
+  uint2* queue;           // [NB][O][QG][QCAP] rings of entries {f(aip), i}
+  uint32_t* qcnt;         // [NB][O][QG] x kBinPad: entries ever reserved (monotone per launch)
+  uint32_t* sync;         // [2 NB] x kBinPad: rounds published per buffer, then owners done; zeroed
+  uint32_t O;             // owners = F << lg_ngrp (<= gridDim.x)
+  uint32_t lg_ngrp;       // word groups per ATV (log2)
+  uint32_t lg_wg;         // words per group (log2)
+  uint32_t tile_bytes;    // packets per CTA per round x 8
+  unsigned long long* prof;  // optional per-CTA phase cycle counters [G][16] (tools; may be null)
+};
+
+// slice words of one owner: r rows x 2^c ATVs x WG words
+__host__ __device__ constexpr size_t own_smem_bytes(uint32_t O, uint32_t slice_words, uint32_t tile_bytes) {
+  return (size_t)kOwnRing * tile_bytes + 2 * (size_t)O * kOwnStride * 8 + 2 * (((size_t)O * 4 + 15) & ~(size_t)15) +
+         16 + (size_t)slice_words * 4;
+}
+
+__device__ __forceinline__ void sts64_if(bool pred, uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.shared.v2.u32 [%1], {%2, %3};\n}"
+               :: "r"((uint32_t)pred), "r"(addr), "r"(a), "r"(b) : "memory");
+}
+
+// owner-side SetAT of one entry {h = f(aip), i}: the r = 4 column windows of
+// L = h >> u, word (i >> 5) mod WG of each ATV, touch bit of i
+template <int CB>
+__device__ __forceinline__ void own_apply(const ScanParams& p, uint32_t* sbm, uint32_t lg_wg, uint32_t h, uint32_t i) {
+  const uint64_t L = (uint64_t)(h >> p.u);
+  const uint64_t D = L | (L << p.W);
+  const uint32_t sub = (i >> 5) & ((1u << lg_wg) - 1u);
+  const uint32_t bit = 1u << touch_bit<CB>(i);
+#pragma unroll
+  for (int y = 0; y < 4; ++y) {
+    const uint32_t x = (uint32_t)(D >> p.shift[y]) & p.cmask;
+#if ASSE_OWN_CHECK
+    uint32_t* a = sbm + (((((uint32_t)y << p.c) | x) << lg_wg) | sub);
+    if (!(*reinterpret_cast<volatile uint32_t*>(a) & bit)) atomicOr(a, bit);
+#else
+    atomicOr(sbm + (((((uint32_t)y << p.c) | x) << lg_wg) | sub), bit);
+#endif
+  }
+}
+
+// Bin two packets: f(aip), BH(bip), owner, one slot atomic each, one 8-byte store each.
+// A full bin (rare) applies the packet straight to the global bitmap (k_scan's REDs).
+// Called by whole warps; lanes with !valid do nothing.
+template <int CB, bool MP>
+__device__ __forceinline__ void own_bin_two(const OwnScanParams& op, const uint4 v, bool valid, uint32_t stg_s,
+                                            uint32_t scount_s, uint32_t scount_dummy) {
+  const ScanParams& p = op.sp;
+  const uint32_t h0 = MP ? walk_mod_p(p.A, v.x) : (uint32_t)p.A * v.x;   // f(aip)
+  const uint32_t h1 = MP ? walk_mod_p(p.A, v.z) : (uint32_t)p.A * v.z;
+  const uint32_t i0 = bh_index(v.y, p.kbh, p.g);                          // BH (A13)
+  const uint32_t i1 = bh_index(v.w, p.kbh, p.g);
+  const uint32_t gs = 5u + op.lg_wg;
+  const uint32_t o0 = ((h0 & p.fmask) << op.lg_ngrp) | (i0 >> gs);
+  const uint32_t o1 = ((h1 & p.fmask) << op.lg_ngrp) | (i1 >> gs);
+  const uint32_t pos0 = atoms_inc(valid ? scount_s + 4u * o0 : scount_dummy);
+  const uint32_t pos1 = atoms_inc(valid ? scount_s + 4u * o1 : scount_dummy);
+  const bool ok0 = pos0 < (uint32_t)kOwnCap, ok1 = pos1 < (uint32_t)kOwnCap;
+  sts64_if(valid && ok0, stg_s + 8u * (o0 * kOwnStride + pos0), h0, i0);
+  sts64_if(valid && ok1, stg_s + 8u * (o1 * kOwnStride + pos1), h1, i1);
+  const bool ov0 = valid && !ok0, ov1 = valid && !ok1;
+  if (__any_sync(0xffffffffu, ov0 || ov1)) {
+    if (ov0) scan_pair<CB, MP>(p, v.x, v.y);
+    if (ov1) scan_pair<CB, MP>(p, v.z, v.w);
+  }
+}
+
+template <int CB, bool MP>
+__global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __restrict__ pk, uint64_t n,
+                                                             OwnScanParams op) {
+  const uint32_t kTileBytes = op.tile_bytes;
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int kSig = 8;
+  static_assert(kSig > kBinNB + 1, "signal barrier ring");
+  __shared__ __align__(8) uint64_t full[kOwnRing], empty[kOwnRing], sigbar[kSig];
+  const uint32_t G = gridDim.x, me = blockIdx.x, O = op.O;
+  const uint32_t Op = (O + 3u) & ~3u;
+  uint8_t* ring = smem;
+  uint2* stg = reinterpret_cast<uint2*>(smem + (size_t)kOwnRing * kTileBytes);         // [2][O][STRIDE]
+  uint32_t* scount = reinterpret_cast<uint32_t*>(stg + 2 * (size_t)O * kOwnStride);    // [2][Op]
+  uint32_t* sbm = scount + 2 * Op + 4;           // 4 spare words: dummy bin counter
+  const uint32_t slice_words = (uint32_t)op.sp.r << (op.sp.c + op.lg_wg);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t head = (((uintptr_t)pk) & 15u) ? 1u : 0u;
+  const uint64_t nbody = (n > head) ? n - head : 0;
+  const uint64_t body_bytes = (nbody >> 1) * 16u;
+  const uint64_t n_tiles = (body_bytes + kTileBytes - 1) / kTileBytes;
+  const uint32_t R = (uint32_t)((n_tiles + G - 1) / G);        // rounds; tile of CTA b in round t: t*G + b
+  uint32_t* prod_done = op.sync;
+  uint32_t* cons_done = op.sync + kBinNB * kBinPad;
+  constexpr int kBinT = 32 * kOwnBinWarps;                    // named barrier 1
+  constexpr int kGroupThreads = 32 * (kOwnConsWarps / 2);     // named barriers 2, 3
+  constexpr int kComputeThreads = 32 * (kOwnBinWarps + kOwnConsWarps);   // named barrier 4
+  const bool owner = me < O;
+
+  if (owner)
+    for (uint32_t q = threadIdx.x; q < slice_words; q += blockDim.x) sbm[q] = 0;
+  for (uint32_t q = threadIdx.x; q < 2 * Op; q += blockDim.x) scount[q] = 0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kOwnRing; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kOwnBinWarps);
+    }
+    for (int q = 0; q < kSig; ++q) mbar_init(&sigbar[q], kOwnBinWarps);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const uint8_t* body = reinterpret_cast<const uint8_t*>(pk + head);
+
+  if (warp == kOwnSigWarp) {                     // ---------------- round publication
+    for (uint32_t tf = 0; tf < R; ++tf) {
+      mbar_wait_sleep(&sigbar[tf % kSig], (tf / kSig) & 1u, 400);   // every binning warp wrote round tf
+      if (lane == 0) {
+        __threadfence();                         // cumulative release of those writes
+        atomicAdd(prod_done + (tf % kBinNB) * kBinPad, 1u);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  if (warp == kOwnTmaWarp) {                     // ---------------- packet tiles -> ring
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t i = 0;
+      for (uint32_t t = 0; t < R; ++t) {
+        const uint64_t tile = (uint64_t)t * G + me;
+        if (tile >= n_tiles) break;
+        const uint32_t st = i % kOwnRing;
+        if (i >= (uint32_t)kOwnRing) mbar_wait_sleep(&empty[st], ((i / kOwnRing) - 1) & 1u, 1000);
+        const uint64_t off = tile * (uint64_t)kTileBytes;
+        const uint32_t bytes = (uint32_t)umin64(kTileBytes, body_bytes - off);
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(ring + (size_t)st * kTileBytes, body + off, bytes, &full[st], pol);
+        ++i;
+      }
+    }
+    return;
+  }
+
+  if (warp < (uint32_t)kOwnBinWarps) {           // ---------------- binning + flushing warps
+    const uint32_t tid = threadIdx.x;
+    if (me == 0 && tid == 0) {                   // scalar head / odd tail packets: direct RED
+      if (head && n > 0) scan_pair<CB, MP>(op.sp, pk[0].x, pk[0].y);
+      if (nbody & 1) scan_pair<CB, MP>(op.sp, pk[n - 1].x, pk[n - 1].y);
+    }
+    uint32_t i = 0;
+    unsigned long long pc[3] = {0, 0, 0};
+    long long c0 = clock64(), c1;
+    const uint32_t my_o = warp + kOwnBinWarps * lane;   // owners this lane reserves for
+    for (uint32_t t = 0; t <= R; ++t) {
+      const uint32_t sb = t & 1u, sf = sb ^ 1u;
+      const uint32_t tf = t - 1, bf = tf % kBinNB;
+      uint32_t cnt = 0, off = 0;
+      if (t >= 1 && my_o < O) {
+        // whole 16-B groups: pad the bin with a "no entry" entry up to an even count
+        const uint32_t c = min(scount[sf * Op + my_o], (uint32_t)kOwnCap);
+        cnt = (c + 1u) & ~1u;
+        if (c & 1u) stg[((size_t)sf * O + my_o) * kOwnStride + c] = make_uint2(0u, 0xFFFFFFFFu);
+        if (cnt) off = atomicAdd(op.qcnt + (((size_t)bf * O + my_o) * kBinQG + (me % kBinQG)) * kBinPad, cnt);
+      }
+      c1 = clock64(); pc[1] += c1 - c0; c0 = c1;
+      uint32_t seen = 0;
+      const uint32_t need = O * (t / kBinNB);    // owners that drained round t - NB
+      if (tid == 0 && t >= (uint32_t)kBinNB && t < R) seen = ld_relaxed_gpu(cons_done + (t % kBinNB) * kBinPad);
+      if (t < R) {
+        const uint64_t tile = (uint64_t)t * G + me;
+        if (tile < n_tiles) {
+          const uint32_t st = i % kOwnRing;
+          mbar_wait(&full[st], (i / kOwnRing) & 1u);
+          const uint32_t n4 = (uint32_t)umin64(kTileBytes, body_bytes - tile * (uint64_t)kTileBytes) >> 4;
+          const uint4* tp = reinterpret_cast<const uint4*>(ring + (size_t)st * kTileBytes);
+          const uint32_t stg_s = smem_u32(stg + (size_t)sb * O * kOwnStride), scount_s = smem_u32(scount + sb * Op);
+          const uint32_t dummy_s = smem_u32(scount + 2 * Op);
+          for (uint32_t q0 = tid - lane; q0 < n4; q0 += kBinT) {   // warp-uniform trip count
+            const uint32_t q = q0 + lane;
+            const bool valid = q < n4;
+            own_bin_two<CB, MP>(op, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s, dummy_s);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
+          ++i;
+        }
+      }
+      c1 = clock64(); pc[0] += c1 - c0; c0 = c1;
+      if (t >= 1) {
+        const uint2* stg_f = stg + (size_t)sf * O * kOwnStride;
+        uint2* qb = op.queue + ((size_t)bf * O * kBinQG + (me % kBinQG)) * kOwnQCap;
+        // two owners per step (one per half-warp), 16 B (two entries) per lane
+        const uint32_t hl = lane & 15u, hw = lane >> 4;
+        constexpr int NS = (kOwnMaxOwners + 2 * kOwnBinWarps - 1) / (2 * kOwnBinWarps);
+        __syncwarp();                            // padding entries written by other lanes
+        uint4 v[NS];
+        uint32_t c2[NS], of[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          c2[k] = __shfl_sync(0xffffffffu, cnt, 2 * k + hw);   // entries (even); 0 beyond O
+          of[k] = __shfl_sync(0xffffffffu, off, 2 * k + hw);
+          const uint32_t ow = warp + kOwnBinWarps * (2 * k + hw);
+          if (2 * hl < c2[k]) {
+            const uint32_t a = smem_u32(stg_f + (size_t)ow * kOwnStride) + 16u * hl;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w) : "r"(a));
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const uint32_t ow = warp + kOwnBinWarps * (2 * k + hw);
+          if (2 * hl < c2[k]) {
+            uint4* dst = reinterpret_cast<uint4*>(qb + (size_t)ow * kBinQG * kOwnQCap);
+            dst[((of[k] >> 1) + hl) & (kOwnQCap / 2 - 1)] = v[k];
+          }
+        }
+        if (my_o < O) scount[sf * Op + my_o] = 0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sigbar[tf % kSig]);   // this warp wrote round tf
+      }
+      if (tid == 0 && t >= (uint32_t)kBinNB && t < R && seen < need)
+        spin_until_geq(cons_done + (t % kBinNB) * kBinPad, need);   // round t-NB drained by every owner
+      named_bar(1, kBinT);                       // bins of round t final; staging sf and counts reusable
+      c1 = clock64(); pc[2] += c1 - c0; c0 = c1;
+    }
+    if (op.prof && tid == 0)
+      for (int q = 0; q < 3; ++q) op.prof[me * 16 + q] = pc[q];
+  } else if (owner) {                            // ---------------- queue-draining warps
+    const uint32_t cid = warp - kOwnConsWarp0;
+    const uint32_t grp = cid / (kOwnConsWarps / 2);
+    const uint32_t gtid = threadIdx.x - 32 * (kOwnConsWarp0 + grp * (kOwnConsWarps / 2));
+    constexpr uint32_t GT = 32 * (kOwnConsWarps / 2);
+    uint32_t last[2][kBinQG];                    // this group's buffers b = grp and grp + 2
+#pragma unroll
+    for (int g = 0; g < (int)kBinQG; ++g) last[0][g] = last[1][g] = 0;
+    unsigned long long cwait = 0, cwork = 0;
+    long long c0 = clock64(), c1;
+    for (uint32_t t = grp; t < R; t += 2) {
+      const uint32_t b = t % kBinNB, li = (t >> 1) & 1u;
+      if (gtid == 0) spin_until_geq(prod_done + b * kBinPad, G * (t / kBinNB + 1), 300);
+      named_bar(2 + grp, kGroupThreads);
+      c1 = clock64(); cwait += c1 - c0; c0 = c1;
+      uint32_t st[kBinQG], len[kBinQG], mx = 0;
+#pragma unroll
+      for (int g = 0; g < (int)kBinQG; ++g) {
+        const uint32_t end = ld_cg_u32(op.qcnt + (((size_t)b * O + me) * kBinQG + g) * kBinPad);
+        const uint32_t s0 = li ? last[1][g] : last[0][g];
+        st[g] = s0;
+        len[g] = end - s0;                       // entries (even)
+        mx = max(mx, len[g]);
+        if (li) last[1][g] = end; else last[0][g] = end;
+      }
+      const uint4* qb4 = reinterpret_cast<const uint4*>(op.queue + ((size_t)b * O + me) * kBinQG * kOwnQCap);
+      constexpr int U = ASSE_OWN_U;              // 16-B groups in flight per thread per ring
+      for (uint32_t e0 = gtid; 2 * e0 < mx; e0 += U * GT) {
+        uint4 v[kBinQG][U];
+#pragma unroll
+        for (int g = 0; g < (int)kBinQG; ++g)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t e = e0 + u * GT;      // 16-B group index within the round's range
+            v[g][u] = make_uint4(0u, ~0u, 0u, ~0u);
+            if (2 * e < len[g]) {
+              const uint4* a = qb4 + g * (kOwnQCap / 2) + (((st[g] >> 1) + e) & (kOwnQCap / 2 - 1));
+              asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(v[g][u].x), "=r"(v[g][u].y), "=r"(v[g][u].z), "=r"(v[g][u].w) : "l"(a));
+            }
+          }
+#pragma unroll
+        for (int g = 0; g < (int)kBinQG; ++g)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint4 x = v[g][u];
+            if (x.y != ~0u) own_apply<CB>(op.sp, sbm, op.lg_wg, x.x, x.y);
+            if (x.w != ~0u) own_apply<CB>(op.sp, sbm, op.lg_wg, x.z, x.w);
+          }
+      }
+      named_bar(2 + grp, kGroupThreads);
+      if (gtid == 0) atomicAdd(cons_done + b * kBinPad, 1u);   // entries consumed before
+      c1 = clock64(); cwork += c1 - c0; c0 = c1;
+    }
+    if (op.prof && gtid == 0) { op.prof[me * 16 + 9 + 2 * grp] = cwait; op.prof[me * 16 + 10 + 2 * grp] = cwork; }
+  }
+  // every round consumed by this CTA (owners) / produced (all): every producer published
+  // every round, so all overflow REDs are performed; OR the owned slice into the global
+  // bitmap: slice word ((y << c | x) << lg_wg) | sub -> global ATV ((y F + z) << c) + x,
+  // word grp * WG + sub
+  named_bar(4, kComputeThreads);
+  if (!owner) return;
+  __threadfence();
+  const ScanParams& p = op.sp;
+  const uint32_t z = me >> op.lg_ngrp, grp = me & ((1u << op.lg_ngrp) - 1u);
+  const uint32_t wg = 1u << op.lg_wg;
+  const uint32_t gbase = (z << p.c) * p.wpa + grp * wg;
+  const uint32_t row_words = (p.fmask + 1u) << p.c;          // ATVs per row
+  if (op.lg_wg >= 1) {                            // 8-B chunks
+    const uint32_t n2 = slice_words >> 1;
+    for (uint32_t q = threadIdx.x; q < n2; q += kComputeThreads) {
+      const uint2 s = reinterpret_cast<const uint2*>(sbm)[q];
+      if (s.x | s.y) {
+        const uint32_t w = q << 1;
+        const uint32_t yx = w >> op.lg_wg, sub = w & (wg - 1u);
+        const uint32_t y = yx >> p.c, x = yx & p.cmask;
+        uint2* gd = reinterpret_cast<uint2*>(p.touch + (size_t)(y * row_words + x) * p.wpa + gbase + sub);
+        uint2 gv;
+        asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(gv.x), "=r"(gv.y) : "l"(gd));
+        gv.x |= s.x; gv.y |= s.y;
+        *gd = gv;
+      }
+    }
+  } else {
+    for (uint32_t q = threadIdx.x; q < slice_words; q += kComputeThreads) {
+      const uint32_t s = sbm[q];
+      if (s) {
+        const uint32_t y = q >> p.c, x = q & p.cmask;
+        uint32_t* gd = p.touch + (size_t)(y * row_words + x) * p.wpa + gbase;
+        *gd = ld_cg_u32(gd) | s;
+      }
+    }
+  }
+}
+
+}  // namespace asse

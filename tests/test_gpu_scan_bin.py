@@ -76,7 +76,8 @@ def test_auto_variant_equals_direct_full_size(cuda_device):
     g = Generator("C5")
     pk = g.slice(0, threads=16)
     rep_a, rep_o = step_both(auto, ora, pk, p["theta"], "C5 auto")
-    assert auto.stats()["scan_bin_launches"] == 1
+    st = auto.stats()
+    assert st["scan_bin_launches"] + st["scan_own_launches"] == 1
     import torch
     d = torch.from_numpy(pk.view(np.int32).reshape(-1)).cuda()
     direct.scan_slice(d)
@@ -89,11 +90,13 @@ def test_auto_variant_equals_direct_full_size(cuda_device):
 def test_variant_validation(cuda_device):
     dev = asse.Asse(**dict(PRESETS["C1"]))
     with pytest.raises(asse.AsseError):
-        dev.set_scan_variant(3)
+        dev.set_scan_variant(4)
     # the paper's geometry (512 MiB touch bitmap) does not fit the shared memories
     big = asse.Asse(**dict(PRESETS["PAPER"]))
     with pytest.raises(asse.AsseError):
         big.set_scan_variant(2)
+    with pytest.raises(asse.AsseError):
+        big.set_scan_variant(3)
     big.set_scan_variant(0)
 
 

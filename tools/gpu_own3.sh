@@ -1,0 +1,17 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_scan_own.py tests/test_gpu_scan_bin.py -x -q --timeout=300 > gpurun_out/own3_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/own3_pytest.log
+L=paper_1807_01527_b200/libasse.so
+cp $L /tmp/libasse_orig.so
+one() {  # name tile workload
+  cp tools/variants/libasse_$1.so $L
+  if [ "$2" = "-" ]; then unset ASSE_SCAN_TILE; else export ASSE_SCAN_TILE=$2; fi
+  timeout 300 python bench.py --workload $3 --steps 20 --warmup 3 --no-e2e --no-cpu --scan-variant 3 > gpurun_out/sw_$1_$2_$3.log 2>&1
+  python -c "import json,sys; d=json.loads(open('gpurun_out/sw_$1_$2_$3.log').read().strip().splitlines()[-1]); print('$1 tile=$2 $3', round(d['value'],2), 'Gpps scan_ms', round(d['roofline']['avg_launch_ms'],4))" 2>&1 | tail -1
+}
+for v in def chk chk14 c12u2; do one $v - C5; done
+for v in def chk; do one $v - C3; one $v - C4; done
+cp tools/variants/libasse_def.so $L
+ASSE_SCAN_PROF=1 timeout 300 python bench.py --workload C5 --steps 3 --warmup 3 --no-e2e --no-cpu --scan-variant 3 2>&1 | grep "k_scan_own" | tail -1
+cp tools/variants/libasse_chk.so $L
+ASSE_SCAN_PROF=1 timeout 300 python bench.py --workload C5 --steps 3 --warmup 3 --no-e2e --no-cpu --scan-variant 3 2>&1 | grep "k_scan_own" | tail -1
+cp /tmp/libasse_orig.so $L
