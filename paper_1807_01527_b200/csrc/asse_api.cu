@@ -373,9 +373,9 @@ static cudaError_t coop_launch_own(Ctx* c, const uint2* pk, uint64_t n, const Ow
 
 static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const ScanParams& sp, cudaStream_t st) {
   const uint32_t G = c->bin_G, O = c->own_O;
-  const size_t sync_words = (2 * kBinNB + (size_t)kBinNB * O * kBinQG) * kBinPad;
+  const size_t sync_words = (2 * kOwnNB + (size_t)kOwnNB * O * kBinQG) * kBinPad;
   if (!c->own_queue) {
-    CK(cudaMalloc(&c->own_queue, (size_t)kBinNB * O * kBinQG * kOwnQCap * sizeof(uint2)));
+    CK(cudaMalloc(&c->own_queue, (size_t)kOwnNB * O * kBinQG * kOwnQCap * sizeof(uint2)));
     CK(cudaMalloc(&c->own_sync, sync_words * 4));
   }
   const int dev = c->device & 63;
@@ -384,7 +384,7 @@ static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const Sc
   OwnScanParams op{};
   op.sp = sp;
   op.queue = c->own_queue;
-  op.qcnt = c->own_sync + 2 * kBinNB * kBinPad;
+  op.qcnt = c->own_sync + 2 * kOwnNB * kBinPad;
   op.sync = c->own_sync;
   op.O = O;
   op.lg_ngrp = c->own_lg_ngrp;
@@ -686,7 +686,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
         if (const char* e = getenv("ASSE_SCAN_TILE")) c->own_tile = ((uint32_t)atoi(e) + 255u) / 256u * 256u * 8u;
         const uint64_t slice_words = (uint64_t)p.r << (p.c + c->own_lg_wg);
         c->own_smem = own_smem_bytes(c->own_O, (uint32_t)std::min<uint64_t>(slice_words, 1u << 30), c->own_tile);
-        c->own_ok = coop && p.r == 4 && (1u << lg_wpa) == c->wpa && c->own_O <= (uint32_t)c->sms &&
+        c->own_ok = coop && p.r == 4 && (1u << lg_wpa) == c->wpa && c->own_O <= (uint32_t)c->sms && c->own_lg_wg <= p.u &&
                     c->own_O <= kOwnMaxOwners && c->own_O >= 2 &&
                     (uint64_t)((c->sms + kBinQG - 1) / kBinQG) * kOwnCap <= kOwnQCap &&
                     slice_words <= (1u << 20) && c->own_smem + 2048 <= (size_t)optin &&

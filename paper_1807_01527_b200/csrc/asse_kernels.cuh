@@ -27,12 +27,22 @@ constexpr int kMaxWorld = 16;  // ranks supported by the peer merge
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ uint32_t bh_index(uint32_t bip, uint64_t kbh, uint32_t g) {
-  // BH (A13): SplitMix64 finalizer of bip ^ K_bh, multiply-shift to [0, g)
-  uint64_t z = (uint64_t)bip ^ kbh;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-  z ^= z >> 31;
-  return (uint32_t)(((z >> 32) * (uint64_t)g) >> 32);
+  // BH (A13): SplitMix64 finalizer of bip ^ K_bh, multiply-shift to [0, g):
+  //   z = bip ^ K; z = (z ^ z>>30) * C1; z = (z ^ z>>27) * C2; z ^= z>>31; i = ((z>>32) * g) >> 32
+  // in 32-bit halves: the high half of bip ^ K is K's (a warp-uniform constant, so the
+  // compiler hoists everything that depends on it), and only the high half of the last
+  // product is needed (bit-identical to the 64-bit form; every pool parity test checks it)
+  constexpr uint32_t C1L = 0x1CE4E5B9u, C1H = 0xBF58476Du, C2L = 0x133111EBu, C2H = 0x94D049BBu;
+  const uint32_t khi = (uint32_t)(kbh >> 32);
+  const uint32_t lo = bip ^ (uint32_t)kbh;
+  const uint32_t xl = lo ^ __funnelshift_r(lo, khi, 30);
+  const uint32_t xh = khi ^ (khi >> 30);
+  const uint32_t yl = xl * C1L;
+  const uint32_t yh = __umulhi(xl, C1L) + xl * C1H + xh * C1L;
+  const uint32_t wl = yl ^ __funnelshift_r(yl, yh, 27);
+  const uint32_t wh = yh ^ (yh >> 27);
+  const uint32_t vh = __umulhi(wl, C2L) + wl * C2H + wh * C2L;
+  return __umulhi(vh ^ (vh >> 31), g);
 }
 
 // Bit position of AT i inside touch word i>>5. Lane l of k_fold owns ATs

@@ -12,7 +12,7 @@
 //
 // At the C3-C5 geometry (F = 16 frames, 2^c = 4096, g = 512: 16 words per ATV) NGRP = 8,
 // WG = 2: 128 owners of 128 KiB each. The producer computes f(aip) and BH(bip), takes one
-// slot in the owner's bin and stores the 8-byte entry {f(aip), i}; the owner derives the r
+// slot in the owner's bin and stores an 8-byte entry (L, word, touch mask); the owner derives the r
 // column windows itself and applies the r SetATs with shared-memory atomics.
 // Per packet: 1 slot atomic (k_scan_bin: 3), 8 B through the L2 queues (12 B + a RED), no
 // global RED. CTAs beyond the O owners produce only.
@@ -34,6 +34,12 @@ namespace asse {
 #ifndef ASSE_OWN_CHECK
 #define ASSE_OWN_CHECK 0
 #endif
+#ifndef ASSE_OWN_NB
+#define ASSE_OWN_NB 8
+#endif
+#ifndef ASSE_OWN_NGR
+#define ASSE_OWN_NGR 2
+#endif
 #ifndef ASSE_OWN_U
 #define ASSE_OWN_U 1
 #endif
@@ -49,6 +55,10 @@ constexpr int kOwnRing = 2;                                // packet-tile ring s
 constexpr int kOwnCap = 30;                                // staged entries per (owner, round) in a CTA
 constexpr int kOwnStride = 30;                             // entries (8 B) between bins: 240 B, 16-B aligned;
                                                            // bin o starts at bank 28o mod 32
+constexpr uint32_t kOwnNB = ASSE_OWN_NB;                   // queue buffers (rounds) in flight (C5: 4 -> 0.952 ms,
+                                                           // 6 0.942, 8 0.927; tools/gpu_own_sweep4.sh)
+constexpr uint32_t kOwnNGR = ASSE_OWN_NGR;                 // drain groups (round t -> group t mod NGR)
+static_assert(kOwnNB % kOwnNGR == 0 && kOwnConsWarps % kOwnNGR == 0, "drain groups");
 constexpr uint32_t kOwnQCap = 2048;                        // ring entries per (buffer, owner, group)
                                                            // >= ceil(G / QG) * kOwnCap
 constexpr uint32_t kOwnMaxOwners = 128;                   // F * NGRP: a power of two <= the SMs
@@ -56,7 +66,7 @@ constexpr uint32_t kOwnMinTilesPerCta = 8;                 // below: k_scan is u
 
 struct OwnScanParams {
   ScanParams sp;          // hashing parameters and the global touch bitmap
-  uint2* queue;           // [NB][O][QG][QCAP] rings of entries {f(aip), i}
+  uint2* queue;           // [NB][O][QG][QCAP] rings of entries (see own_bin_two)
   uint32_t* qcnt;         // [NB][O][QG] x kBinPad: entries ever reserved (monotone per launch)
   uint32_t* sync;         // [2 NB] x kBinPad: rounds published per buffer, then owners done; zeroed
   uint32_t O;             // owners = F << lg_ngrp (<= gridDim.x)
@@ -72,34 +82,59 @@ __host__ __device__ constexpr size_t own_smem_bytes(uint32_t O, uint32_t slice_w
          16 + (size_t)slice_words * 4;
 }
 
+#ifndef ASSE_OWN_SPIN
+#define ASSE_OWN_SPIN 1
+#endif
+#ifndef ASSE_OWN_POLL_NS
+#define ASSE_OWN_POLL_NS 1
+#endif
+// mbarrier wait for warps off the critical path: the hardware suspends the thread until
+// the phase completes or the hint (ns) expires, so the wait costs no issue slots (a
+// nanosleep poll loop cost ~8 % of the kernel's instructions, ncu r01g)
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t phase) {
+#if ASSE_OWN_SPIN
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done) : "r"(smem_u32(bar)), "r"(phase), "r"(1000000u) : "memory");
+  }
+#else
+  mbar_wait_sleep(bar, phase, 1000);
+#endif
+}
+
 __device__ __forceinline__ void sts64_if(bool pred, uint32_t addr, uint32_t a, uint32_t b) {
   asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.shared.v2.u32 [%1], {%2, %3};\n}"
                :: "r"((uint32_t)pred), "r"(addr), "r"(a), "r"(b) : "memory");
 }
 
-// owner-side SetAT of one entry {h = f(aip), i}: the r = 4 column windows of
-// L = h >> u, word (i >> 5) mod WG of each ATV, touch bit of i
-template <int CB>
-__device__ __forceinline__ void own_apply(const ScanParams& p, uint32_t* sbm, uint32_t lg_wg, uint32_t h, uint32_t i) {
-  const uint64_t L = (uint64_t)(h >> p.u);
+// owner-side SetAT of one entry {e = (f(aip) with its frame bits replaced by the word
+// within the group), m = touch-bit mask of i}: the r = 4 column windows of
+// L = f(aip) >> u, word `sub` of the group in each ATV
+__device__ __forceinline__ void own_apply(const ScanParams& p, uint32_t* sbm, uint32_t lg_wg, uint32_t e, uint32_t m) {
+  const uint64_t L = (uint64_t)(e >> p.u);
   const uint64_t D = L | (L << p.W);
-  const uint32_t sub = (i >> 5) & ((1u << lg_wg) - 1u);
-  const uint32_t bit = 1u << touch_bit<CB>(i);
+  const uint32_t sub = e & p.fmask;
 #pragma unroll
   for (int y = 0; y < 4; ++y) {
     const uint32_t x = (uint32_t)(D >> p.shift[y]) & p.cmask;
 #if ASSE_OWN_CHECK
     uint32_t* a = sbm + (((((uint32_t)y << p.c) | x) << lg_wg) | sub);
-    if (!(*reinterpret_cast<volatile uint32_t*>(a) & bit)) atomicOr(a, bit);
+    if (!(*reinterpret_cast<volatile uint32_t*>(a) & m)) atomicOr(a, m);
 #else
-    atomicOr(sbm + (((((uint32_t)y << p.c) | x) << lg_wg) | sub), bit);
+    atomicOr(sbm + (((((uint32_t)y << p.c) | x) << lg_wg) | sub), m);
 #endif
   }
 }
 
 // Bin two packets: f(aip), BH(bip), owner, one slot atomic each, one 8-byte store each.
-// A full bin (rare) applies the packet straight to the global bitmap (k_scan's REDs).
-// Called by whole warps; lanes with !valid do nothing.
+// The entry carries what the owner needs and nothing it knows: the LBS L in the
+// high 32-u bits, the word within the owner's group (< 2^u, host-checked) in the frame
+// bits, and the touch-bit mask of i. A full bin (rare) applies the packet straight to the
+// global bitmap (k_scan's REDs). Called by whole warps; lanes with !valid do nothing.
 template <int CB, bool MP>
 __device__ __forceinline__ void own_bin_two(const OwnScanParams& op, const uint4 v, bool valid, uint32_t stg_s,
                                             uint32_t scount_s, uint32_t scount_dummy) {
@@ -108,14 +143,16 @@ __device__ __forceinline__ void own_bin_two(const OwnScanParams& op, const uint4
   const uint32_t h1 = MP ? walk_mod_p(p.A, v.z) : (uint32_t)p.A * v.z;
   const uint32_t i0 = bh_index(v.y, p.kbh, p.g);                          // BH (A13)
   const uint32_t i1 = bh_index(v.w, p.kbh, p.g);
-  const uint32_t gs = 5u + op.lg_wg;
+  const uint32_t gs = 5u + op.lg_wg, wgm = (1u << op.lg_wg) - 1u;
   const uint32_t o0 = ((h0 & p.fmask) << op.lg_ngrp) | (i0 >> gs);
   const uint32_t o1 = ((h1 & p.fmask) << op.lg_ngrp) | (i1 >> gs);
   const uint32_t pos0 = atoms_inc(valid ? scount_s + 4u * o0 : scount_dummy);
   const uint32_t pos1 = atoms_inc(valid ? scount_s + 4u * o1 : scount_dummy);
   const bool ok0 = pos0 < (uint32_t)kOwnCap, ok1 = pos1 < (uint32_t)kOwnCap;
-  sts64_if(valid && ok0, stg_s + 8u * (o0 * kOwnStride + pos0), h0, i0);
-  sts64_if(valid && ok1, stg_s + 8u * (o1 * kOwnStride + pos1), h1, i1);
+  sts64_if(valid && ok0, stg_s + 8u * (o0 * kOwnStride + pos0), (h0 & ~p.fmask) | ((i0 >> 5) & wgm),
+           1u << touch_bit<CB>(i0));
+  sts64_if(valid && ok1, stg_s + 8u * (o1 * kOwnStride + pos1), (h1 & ~p.fmask) | ((i1 >> 5) & wgm),
+           1u << touch_bit<CB>(i1));
   const bool ov0 = valid && !ok0, ov1 = valid && !ok1;
   if (__any_sync(0xffffffffu, ov0 || ov1)) {
     if (ov0) scan_pair<CB, MP>(p, v.x, v.y);
@@ -128,9 +165,10 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
                                                              OwnScanParams op) {
   const uint32_t kTileBytes = op.tile_bytes;
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int kSig = 8;
-  static_assert(kSig > kBinNB + 1, "signal barrier ring");
+  constexpr int kSig = 2 * kOwnNB;
+  static_assert(kSig > kOwnNB + 1, "signal barrier ring");
   __shared__ __align__(8) uint64_t full[kOwnRing], empty[kOwnRing], sigbar[kSig];
+  __shared__ uint32_t slast[kOwnNB][kBinQG];     // drain: end of the last drained round per buffer/ring
   const uint32_t G = gridDim.x, me = blockIdx.x, O = op.O;
   const uint32_t Op = (O + 3u) & ~3u;
   uint8_t* ring = smem;
@@ -145,10 +183,10 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   const uint64_t n_tiles = (body_bytes + kTileBytes - 1) / kTileBytes;
   const uint32_t R = (uint32_t)((n_tiles + G - 1) / G);        // rounds; tile of CTA b in round t: t*G + b
   uint32_t* prod_done = op.sync;
-  uint32_t* cons_done = op.sync + kBinNB * kBinPad;
+  uint32_t* cons_done = op.sync + kOwnNB * kBinPad;
   constexpr int kBinT = 32 * kOwnBinWarps;                    // named barrier 1
-  constexpr int kGroupThreads = 32 * (kOwnConsWarps / 2);     // named barriers 2, 3
-  constexpr int kComputeThreads = 32 * (kOwnBinWarps + kOwnConsWarps);   // named barrier 4
+  constexpr int kGroupThreads = 32 * (kOwnConsWarps / kOwnNGR);   // named barriers 2 .. 1 + NGR
+  constexpr int kComputeThreads = 32 * (kOwnBinWarps + kOwnConsWarps);   // named barrier 8
   const bool owner = me < O;
 
   if (owner)
@@ -167,10 +205,10 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
 
   if (warp == kOwnSigWarp) {                     // ---------------- round publication
     for (uint32_t tf = 0; tf < R; ++tf) {
-      mbar_wait_sleep(&sigbar[tf % kSig], (tf / kSig) & 1u, 400);   // every binning warp wrote round tf
+      mbar_wait_suspend(&sigbar[tf % kSig], (tf / kSig) & 1u);   // every binning warp wrote round tf
       if (lane == 0) {
         __threadfence();                         // cumulative release of those writes
-        atomicAdd(prod_done + (tf % kBinNB) * kBinPad, 1u);
+        atomicAdd(prod_done + (tf % kOwnNB) * kBinPad, 1u);
       }
       __syncwarp();
     }
@@ -184,7 +222,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         const uint64_t tile = (uint64_t)t * G + me;
         if (tile >= n_tiles) break;
         const uint32_t st = i % kOwnRing;
-        if (i >= (uint32_t)kOwnRing) mbar_wait_sleep(&empty[st], ((i / kOwnRing) - 1) & 1u, 1000);
+        if (i >= (uint32_t)kOwnRing) mbar_wait_suspend(&empty[st], ((i / kOwnRing) - 1) & 1u);
         const uint64_t off = tile * (uint64_t)kTileBytes;
         const uint32_t bytes = (uint32_t)umin64(kTileBytes, body_bytes - off);
         mbar_expect_tx(&full[st], bytes);
@@ -207,19 +245,19 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
     const uint32_t my_o = warp + kOwnBinWarps * lane;   // owners this lane reserves for
     for (uint32_t t = 0; t <= R; ++t) {
       const uint32_t sb = t & 1u, sf = sb ^ 1u;
-      const uint32_t tf = t - 1, bf = tf % kBinNB;
+      const uint32_t tf = t - 1, bf = tf % kOwnNB;
       uint32_t cnt = 0, off = 0;
       if (t >= 1 && my_o < O) {
         // whole 16-B groups: pad the bin with a "no entry" entry up to an even count
         const uint32_t c = min(scount[sf * Op + my_o], (uint32_t)kOwnCap);
         cnt = (c + 1u) & ~1u;
-        if (c & 1u) stg[((size_t)sf * O + my_o) * kOwnStride + c] = make_uint2(0u, 0xFFFFFFFFu);
+        if (c & 1u) stg[((size_t)sf * O + my_o) * kOwnStride + c] = make_uint2(0u, 0u);   // mask 0: no entry
         if (cnt) off = atomicAdd(op.qcnt + (((size_t)bf * O + my_o) * kBinQG + (me % kBinQG)) * kBinPad, cnt);
       }
       c1 = clock64(); pc[1] += c1 - c0; c0 = c1;
       uint32_t seen = 0;
-      const uint32_t need = O * (t / kBinNB);    // owners that drained round t - NB
-      if (tid == 0 && t >= (uint32_t)kBinNB && t < R) seen = ld_relaxed_gpu(cons_done + (t % kBinNB) * kBinPad);
+      const uint32_t need = O * (t / kOwnNB);    // owners that drained round t - NB
+      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R) seen = ld_relaxed_gpu(cons_done + (t % kOwnNB) * kBinPad);
       if (t < R) {
         const uint64_t tile = (uint64_t)t * G + me;
         if (tile < n_tiles) {
@@ -272,8 +310,8 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         __syncwarp();
         if (lane == 0) mbar_arrive(&sigbar[tf % kSig]);   // this warp wrote round tf
       }
-      if (tid == 0 && t >= (uint32_t)kBinNB && t < R && seen < need)
-        spin_until_geq(cons_done + (t % kBinNB) * kBinPad, need);   // round t-NB drained by every owner
+      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R && seen < need)
+        spin_until_geq(cons_done + (t % kOwnNB) * kBinPad, need, 128 * ASSE_OWN_POLL_NS);   // round t-NB drained
       named_bar(1, kBinT);                       // bins of round t final; staging sf and counts reusable
       c1 = clock64(); pc[2] += c1 - c0; c0 = c1;
     }
@@ -281,28 +319,25 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       for (int q = 0; q < 3; ++q) op.prof[me * 16 + q] = pc[q];
   } else if (owner) {                            // ---------------- queue-draining warps
     const uint32_t cid = warp - kOwnConsWarp0;
-    const uint32_t grp = cid / (kOwnConsWarps / 2);
-    const uint32_t gtid = threadIdx.x - 32 * (kOwnConsWarp0 + grp * (kOwnConsWarps / 2));
-    constexpr uint32_t GT = 32 * (kOwnConsWarps / 2);
-    uint32_t last[2][kBinQG];                    // this group's buffers b = grp and grp + 2
-#pragma unroll
-    for (int g = 0; g < (int)kBinQG; ++g) last[0][g] = last[1][g] = 0;
+    const uint32_t grp = cid / (kOwnConsWarps / kOwnNGR);
+    const uint32_t gtid = threadIdx.x - 32 * (kOwnConsWarp0 + grp * (kOwnConsWarps / kOwnNGR));
+    constexpr uint32_t GT = 32 * (kOwnConsWarps / kOwnNGR);
     unsigned long long cwait = 0, cwork = 0;
     long long c0 = clock64(), c1;
-    for (uint32_t t = grp; t < R; t += 2) {
-      const uint32_t b = t % kBinNB, li = (t >> 1) & 1u;
-      if (gtid == 0) spin_until_geq(prod_done + b * kBinPad, G * (t / kBinNB + 1), 300);
+    for (uint32_t t = grp; t < R; t += kOwnNGR) {
+      const uint32_t b = t % kOwnNB;
+      if (gtid == 0) spin_until_geq(prod_done + b * kBinPad, G * (t / kOwnNB + 1), 300 * ASSE_OWN_POLL_NS);
       named_bar(2 + grp, kGroupThreads);
       c1 = clock64(); cwait += c1 - c0; c0 = c1;
-      uint32_t st[kBinQG], len[kBinQG], mx = 0;
+      // the round's entries: QG ranges [start, end) of the owner's rings of buffer b; start =
+      // end of the previous round in this buffer (slast, written by this group only)
+      uint32_t st[kBinQG], len[kBinQG], en[kBinQG], mx = 0;
 #pragma unroll
       for (int g = 0; g < (int)kBinQG; ++g) {
-        const uint32_t end = ld_cg_u32(op.qcnt + (((size_t)b * O + me) * kBinQG + g) * kBinPad);
-        const uint32_t s0 = li ? last[1][g] : last[0][g];
-        st[g] = s0;
-        len[g] = end - s0;                       // entries (even)
+        en[g] = ld_cg_u32(op.qcnt + (((size_t)b * O + me) * kBinQG + g) * kBinPad);
+        st[g] = t >= kOwnNB ? slast[b][g] : 0u;
+        len[g] = en[g] - st[g];                  // entries (even)
         mx = max(mx, len[g]);
-        if (li) last[1][g] = end; else last[0][g] = end;
       }
       const uint4* qb4 = reinterpret_cast<const uint4*>(op.queue + ((size_t)b * O + me) * kBinQG * kOwnQCap);
       constexpr int U = ASSE_OWN_U;              // 16-B groups in flight per thread per ring
@@ -313,7 +348,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint32_t e = e0 + u * GT;      // 16-B group index within the round's range
-            v[g][u] = make_uint4(0u, ~0u, 0u, ~0u);
+            v[g][u] = make_uint4(0u, 0u, 0u, 0u);
             if (2 * e < len[g]) {
               const uint4* a = qb4 + g * (kOwnQCap / 2) + (((st[g] >> 1) + e) & (kOwnQCap / 2 - 1));
               asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -325,21 +360,25 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint4 x = v[g][u];
-            if (x.y != ~0u) own_apply<CB>(op.sp, sbm, op.lg_wg, x.x, x.y);
-            if (x.w != ~0u) own_apply<CB>(op.sp, sbm, op.lg_wg, x.z, x.w);
+            if (x.y) own_apply(op.sp, sbm, op.lg_wg, x.x, x.y);
+            if (x.w) own_apply(op.sp, sbm, op.lg_wg, x.z, x.w);
           }
       }
       named_bar(2 + grp, kGroupThreads);
-      if (gtid == 0) atomicAdd(cons_done + b * kBinPad, 1u);   // entries consumed before
+      if (gtid == 0) {
+        atomicAdd(cons_done + b * kBinPad, 1u);  // entries consumed before
+#pragma unroll
+        for (int g = 0; g < (int)kBinQG; ++g) slast[b][g] = en[g];
+      }
       c1 = clock64(); cwork += c1 - c0; c0 = c1;
     }
-    if (op.prof && gtid == 0) { op.prof[me * 16 + 9 + 2 * grp] = cwait; op.prof[me * 16 + 10 + 2 * grp] = cwork; }
+    if (op.prof && gtid == 0 && grp < 2) { op.prof[me * 16 + 9 + 2 * grp] = cwait; op.prof[me * 16 + 10 + 2 * grp] = cwork; }
   }
   // every round consumed by this CTA (owners) / produced (all): every producer published
   // every round, so all overflow REDs are performed; OR the owned slice into the global
   // bitmap: slice word ((y << c | x) << lg_wg) | sub -> global ATV ((y F + z) << c) + x,
   // word grp * WG + sub
-  named_bar(4, kComputeThreads);
+  named_bar(8, kComputeThreads);
   if (!owner) return;
   __threadfence();
   const ScanParams& p = op.sp;
