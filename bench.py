@@ -62,6 +62,15 @@ def load_l2_peak():
         return None
 
 
+def load_smem_peak():
+    """Measured random shared-memory atomic peak (tools/smembench.cu), chip-wide lane-ops/s."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "smem_atomic_peak.json")) as f:
+            return float(json.load(f)["atom_shared_or_glane_ops"]) * 1e9
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """NVML sampling of SM clocks and clock-event reasons during the timed region."""
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -316,6 +325,7 @@ def main():
     binned = sb["scan_bin_launches"] > sa["scan_bin_launches"]
     owned = sb["scan_own_launches"] > sa["scan_own_launches"]
     scan_kernel = "k_scan_own" if owned else "k_scan_bin" if binned else "k_scan"
+    smem_ops = (1 + p["r"]) if owned else 2 * (p["r"] - st1["scan_rows_red"]) if binned else 0
     peak, peak_src = load_peaks()
     scan_bytes = n_local * (8 + p["r"] * cb)          # 8 B read + r codes written
     scan_gbs = scan_bytes / (scan_launch_ms / 1e3) / 1e9
@@ -410,6 +420,12 @@ def main():
                                "frac_of_l2_random_red_ceiling": (p["r"] * n_local / (scan_launch_ms / 1e3))
                                / load_l2_peak() if load_l2_peak() else None,
                                "rows_via_red": 0 if owned else st1["scan_rows_red"] if binned else p["r"],
+                               # shared-memory atomics per packet: k_scan_own 1 slot + r SetATs at the
+                               # owner; k_scan_bin (r - RR) slots + (r - RR) SetATs; k_scan none
+                               "smem_atomics_per_packet": smem_ops,
+                               "smem_atomic_ceiling_glane_ops": (load_smem_peak() or float("nan")) / 1e9,
+                               "frac_of_smem_atomic_ceiling": (smem_ops * n_local / (scan_launch_ms / 1e3))
+                               / load_smem_peak() if load_smem_peak() and smem_ops else None,
                                "peak_source": "profiles/l2_random_peak.json (tools/l2bench.cu, measured)",
                                "note": "k_scan: r red.global.or.b32 per packet, bound by the L2 random-op "
                                        "ceiling; k_scan_bin: rows below rows_via_red take that route, the "
