@@ -356,7 +356,7 @@ static asse_status launch_scan_bin(Ctx* c, const uint2* pk, uint64_t n, const Sc
   return ASSE_OK;
 }
 
-template <int CB, bool MP>
+template <int CB, bool MP, class Geo>
 static cudaError_t coop_launch_own(Ctx* c, const uint2* pk, uint64_t n, const OwnScanParams& op, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(c->bin_G);
@@ -368,7 +368,7 @@ static cudaError_t coop_launch_own(Ctx* c, const uint2* pk, uint64_t n, const Ow
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_scan_own<CB, MP>, pk, n, op);
+  return cudaLaunchKernelEx(&cfg, k_scan_own<CB, MP, Geo>, pk, n, op);
 }
 
 static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const ScanParams& sp, cudaStream_t st) {
@@ -398,8 +398,16 @@ static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const Sc
   }
   CK(cudaMemsetAsync(c->own_sync, 0, sync_words * 4, st));
   cudaError_t e;
-  if (c->cfg.mangle) e = c->cb == 1 ? coop_launch_own<1, true>(c, pk, n, op, st) : coop_launch_own<2, true>(c, pk, n, op, st);
-  else e = c->cb == 1 ? coop_launch_own<1, false>(c, pk, n, op, st) : coop_launch_own<2, false>(c, pk, n, op, st);
+  const asse_config& g = c->cfg;
+  const bool c3 = g.u == 4 && g.c == 12 && g.s == 6 && g.g == 512 && g.r == 4 && c->own_lg_ngrp == 3 && c->own_lg_wg == 1 &&
+                  !getenv("ASSE_SCAN_OWN_GENERIC");   // the BASELINE C3-C5 geometry: constants folded
+  if (c3) {
+    if (g.mangle) e = c->cb == 1 ? coop_launch_own<1, true, GeoC3>(c, pk, n, op, st) : coop_launch_own<2, true, GeoC3>(c, pk, n, op, st);
+    else e = c->cb == 1 ? coop_launch_own<1, false, GeoC3>(c, pk, n, op, st) : coop_launch_own<2, false, GeoC3>(c, pk, n, op, st);
+  } else {
+    if (g.mangle) e = c->cb == 1 ? coop_launch_own<1, true, GeoRt>(c, pk, n, op, st) : coop_launch_own<2, true, GeoRt>(c, pk, n, op, st);
+    else e = c->cb == 1 ? coop_launch_own<1, false, GeoRt>(c, pk, n, op, st) : coop_launch_own<2, false, GeoRt>(c, pk, n, op, st);
+  }
   if (e == cudaErrorCooperativeLaunchTooLarge) {
     cudaGetLastError();
     return ASSE_E_CAPACITY;
@@ -692,11 +700,13 @@ asse_status asse_init(const asse_config* cfg, void** out) {
                     slice_words <= (1u << 20) && c->own_smem + 2048 <= (size_t)optin &&
                     !getenv("ASSE_SCAN_NO_OWN");
         if (c->own_ok) {
-          void* fns[4] = {(void*)k_scan_own<1, false>, (void*)k_scan_own<2, false>, (void*)k_scan_own<1, true>,
-                          (void*)k_scan_own<2, true>};
+          void* fns[8] = {(void*)k_scan_own<1, false, GeoRt>, (void*)k_scan_own<2, false, GeoRt>,
+                          (void*)k_scan_own<1, true, GeoRt>, (void*)k_scan_own<2, true, GeoRt>,
+                          (void*)k_scan_own<1, false, GeoC3>, (void*)k_scan_own<2, false, GeoC3>,
+                          (void*)k_scan_own<1, true, GeoC3>, (void*)k_scan_own<2, true, GeoC3>};
           for (void* f : fns) CKI(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->own_smem));
           int oocc = 0;
-          CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oocc, k_scan_own<1, false>, kOwnThreads, c->own_smem));
+          CKI(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oocc, k_scan_own<1, false, GeoRt>, kOwnThreads, c->own_smem));
           c->own_ok = oocc >= 1;
         }
         c->stats.scan_own_ok = c->own_ok ? 1u : 0u;

@@ -111,21 +111,52 @@ __device__ __forceinline__ void sts64_if(bool pred, uint32_t addr, uint32_t a, u
                :: "r"((uint32_t)pred), "r"(addr), "r"(a), "r"(b) : "memory");
 }
 
+// Geometry seen by the hot loops: runtime values (any geometry own_ok admits) or
+// compile-time constants for the BASELINE C3-C5 geometry (u = 4, c = 12, s = 6, g = 512,
+// NGRP = 8, WG = 2), so shifts, masks and the column-window offsets fold into immediates
+// (ncu r01h: the owner-side SetAT took 36 instructions per entry with runtime values).
+struct GeoRt {
+  __device__ static __forceinline__ uint32_t u(const OwnScanParams& op) { return op.sp.u; }
+  __device__ static __forceinline__ uint32_t W(const OwnScanParams& op) { return op.sp.W; }
+  __device__ static __forceinline__ uint32_t c(const OwnScanParams& op) { return op.sp.c; }
+  __device__ static __forceinline__ uint32_t cmask(const OwnScanParams& op) { return op.sp.cmask; }
+  __device__ static __forceinline__ uint32_t fmask(const OwnScanParams& op) { return op.sp.fmask; }
+  __device__ static __forceinline__ uint32_t g(const OwnScanParams& op) { return op.sp.g; }
+  __device__ static __forceinline__ uint32_t shift(const OwnScanParams& op, int y) { return op.sp.shift[y]; }
+  __device__ static __forceinline__ uint32_t lg_ngrp(const OwnScanParams& op) { return op.lg_ngrp; }
+  __device__ static __forceinline__ uint32_t lg_wg(const OwnScanParams& op) { return op.lg_wg; }
+};
+template <uint32_t U_, uint32_t C_, uint32_t S_, uint32_t G_, uint32_t LGNG_, uint32_t LGWG_>
+struct GeoCt {
+  __device__ static __forceinline__ constexpr uint32_t u(const OwnScanParams&) { return U_; }
+  __device__ static __forceinline__ constexpr uint32_t W(const OwnScanParams&) { return 32u - U_; }
+  __device__ static __forceinline__ constexpr uint32_t c(const OwnScanParams&) { return C_; }
+  __device__ static __forceinline__ constexpr uint32_t cmask(const OwnScanParams&) { return (1u << C_) - 1u; }
+  __device__ static __forceinline__ constexpr uint32_t fmask(const OwnScanParams&) { return (1u << U_) - 1u; }
+  __device__ static __forceinline__ constexpr uint32_t g(const OwnScanParams&) { return G_; }
+  __device__ static __forceinline__ constexpr uint32_t shift(const OwnScanParams&, int y) { return (S_ * y) % (32u - U_); }
+  __device__ static __forceinline__ constexpr uint32_t lg_ngrp(const OwnScanParams&) { return LGNG_; }
+  __device__ static __forceinline__ constexpr uint32_t lg_wg(const OwnScanParams&) { return LGWG_; }
+};
+using GeoC3 = GeoCt<4, 12, 6, 512, 3, 1>;
+
 // owner-side SetAT of one entry {e = (f(aip) with its frame bits replaced by the word
 // within the group), m = touch-bit mask of i}: the r = 4 column windows of
 // L = f(aip) >> u, word `sub` of the group in each ATV
-__device__ __forceinline__ void own_apply(const ScanParams& p, uint32_t* sbm, uint32_t lg_wg, uint32_t e, uint32_t m) {
-  const uint64_t L = (uint64_t)(e >> p.u);
-  const uint64_t D = L | (L << p.W);
-  const uint32_t sub = e & p.fmask;
+template <class Geo>
+__device__ __forceinline__ void own_apply(const OwnScanParams& op, uint32_t* sbm, uint32_t e, uint32_t m) {
+  const uint64_t L = (uint64_t)(e >> Geo::u(op));
+  const uint64_t D = L | (L << Geo::W(op));
+  const uint32_t sub = e & Geo::fmask(op);
 #pragma unroll
   for (int y = 0; y < 4; ++y) {
-    const uint32_t x = (uint32_t)(D >> p.shift[y]) & p.cmask;
+    const uint32_t x = (uint32_t)(D >> Geo::shift(op, y)) & Geo::cmask(op);
+    const uint32_t w = (((((uint32_t)y << Geo::c(op)) | x) << Geo::lg_wg(op)) | sub);
 #if ASSE_OWN_CHECK
-    uint32_t* a = sbm + (((((uint32_t)y << p.c) | x) << lg_wg) | sub);
+    uint32_t* a = sbm + w;
     if (!(*reinterpret_cast<volatile uint32_t*>(a) & m)) atomicOr(a, m);
 #else
-    atomicOr(sbm + (((((uint32_t)y << p.c) | x) << lg_wg) | sub), m);
+    atomicOr(sbm + w, m);
 #endif
   }
 }
@@ -135,23 +166,24 @@ __device__ __forceinline__ void own_apply(const ScanParams& p, uint32_t* sbm, ui
 // high 32-u bits, the word within the owner's group (< 2^u, host-checked) in the frame
 // bits, and the touch-bit mask of i. A full bin (rare) applies the packet straight to the
 // global bitmap (k_scan's REDs). Called by whole warps; lanes with !valid do nothing.
-template <int CB, bool MP>
+template <int CB, bool MP, class Geo>
 __device__ __forceinline__ void own_bin_two(const OwnScanParams& op, const uint4 v, bool valid, uint32_t stg_s,
                                             uint32_t scount_s, uint32_t scount_dummy) {
   const ScanParams& p = op.sp;
   const uint32_t h0 = MP ? walk_mod_p(p.A, v.x) : (uint32_t)p.A * v.x;   // f(aip)
   const uint32_t h1 = MP ? walk_mod_p(p.A, v.z) : (uint32_t)p.A * v.z;
-  const uint32_t i0 = bh_index(v.y, p.kbh, p.g);                          // BH (A13)
-  const uint32_t i1 = bh_index(v.w, p.kbh, p.g);
-  const uint32_t gs = 5u + op.lg_wg, wgm = (1u << op.lg_wg) - 1u;
-  const uint32_t o0 = ((h0 & p.fmask) << op.lg_ngrp) | (i0 >> gs);
-  const uint32_t o1 = ((h1 & p.fmask) << op.lg_ngrp) | (i1 >> gs);
+  const uint32_t i0 = bh_index(v.y, p.kbh, Geo::g(op));                   // BH (A13)
+  const uint32_t i1 = bh_index(v.w, p.kbh, Geo::g(op));
+  const uint32_t gs = 5u + Geo::lg_wg(op), wgm = (1u << Geo::lg_wg(op)) - 1u;
+  const uint32_t fm = Geo::fmask(op);
+  const uint32_t o0 = ((h0 & fm) << Geo::lg_ngrp(op)) | (i0 >> gs);
+  const uint32_t o1 = ((h1 & fm) << Geo::lg_ngrp(op)) | (i1 >> gs);
   const uint32_t pos0 = atoms_inc(valid ? scount_s + 4u * o0 : scount_dummy);
   const uint32_t pos1 = atoms_inc(valid ? scount_s + 4u * o1 : scount_dummy);
   const bool ok0 = pos0 < (uint32_t)kOwnCap, ok1 = pos1 < (uint32_t)kOwnCap;
-  sts64_if(valid && ok0, stg_s + 8u * (o0 * kOwnStride + pos0), (h0 & ~p.fmask) | ((i0 >> 5) & wgm),
+  sts64_if(valid && ok0, stg_s + 8u * (o0 * kOwnStride + pos0), (h0 & ~fm) | ((i0 >> 5) & wgm),
            1u << touch_bit<CB>(i0));
-  sts64_if(valid && ok1, stg_s + 8u * (o1 * kOwnStride + pos1), (h1 & ~p.fmask) | ((i1 >> 5) & wgm),
+  sts64_if(valid && ok1, stg_s + 8u * (o1 * kOwnStride + pos1), (h1 & ~fm) | ((i1 >> 5) & wgm),
            1u << touch_bit<CB>(i1));
   const bool ov0 = valid && !ok0, ov1 = valid && !ok1;
   if (__any_sync(0xffffffffu, ov0 || ov1)) {
@@ -160,7 +192,7 @@ __device__ __forceinline__ void own_bin_two(const OwnScanParams& op, const uint4
   }
 }
 
-template <int CB, bool MP>
+template <int CB, bool MP, class Geo>
 __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __restrict__ pk, uint64_t n,
                                                              OwnScanParams op) {
   const uint32_t kTileBytes = op.tile_bytes;
@@ -270,7 +302,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
           for (uint32_t q0 = tid - lane; q0 < n4; q0 += kBinT) {   // warp-uniform trip count
             const uint32_t q = q0 + lane;
             const bool valid = q < n4;
-            own_bin_two<CB, MP>(op, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s, dummy_s);
+            own_bin_two<CB, MP, Geo>(op, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s, dummy_s);
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[st]);
@@ -360,8 +392,8 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint4 x = v[g][u];
-            if (x.y) own_apply(op.sp, sbm, op.lg_wg, x.x, x.y);
-            if (x.w) own_apply(op.sp, sbm, op.lg_wg, x.z, x.w);
+            if (x.y) own_apply<Geo>(op, sbm, x.x, x.y);
+            if (x.w) own_apply<Geo>(op, sbm, x.z, x.w);
           }
       }
       named_bar(2 + grp, kGroupThreads);
