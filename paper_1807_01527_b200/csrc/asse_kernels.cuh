@@ -611,7 +611,7 @@ __device__ __forceinline__ uint32_t place_row(uint32_t x, uint32_t sh, uint32_t 
 // x_y and tests SA membership — whichever is fewer probes.
 constexpr uint32_t kPartSmem = 2048;   // partial LBS kept in shared memory per level buffer
 
-__global__ void __launch_bounds__(512) k_restore(RestoreParams p) {
+__global__ void __launch_bounds__(512, 2) k_restore(RestoreParams p) {   // 2 CTAs per SM: one wave of F x parts
   extern __shared__ uint32_t s_bits[];  // r * E/32 words of SA(y, z) membership
   __shared__ uint32_t s_part[2][kPartSmem];
   __shared__ uint32_t s_nsa[kMaxR];
