@@ -696,7 +696,8 @@ asse_status asse_init(const asse_config* cfg, void** out) {
         c->own_smem = own_smem_bytes(c->own_O, (uint32_t)std::min<uint64_t>(slice_words, 1u << 30), c->own_tile);
         c->own_ok = coop && p.r == 4 && (1u << lg_wpa) == c->wpa && c->own_O <= (uint32_t)c->sms && c->own_lg_wg <= p.u &&
                     c->own_O <= kOwnMaxOwners && c->own_O >= 2 &&
-                    (uint64_t)((c->sms + kBinQG - 1) / kBinQG) * kOwnCap <= kOwnQCap &&
+                    (uint64_t)((c->own_O + kBinQG - 1) / kBinQG) * kOwnCap +
+                            (uint64_t)((c->sms - c->own_O + kBinQG - 1) / kBinQG) * kOwnCap * kOwnNoTpr <= kOwnQCap &&
                     slice_words <= (1u << 20) && c->own_smem + 2048 <= (size_t)optin &&
                     !getenv("ASSE_SCAN_NO_OWN");
         if (c->own_ok) {

@@ -29,7 +29,7 @@ namespace asse {
 #define ASSE_OWN_BIN_WARPS 16
 #endif
 #ifndef ASSE_OWN_CONS_WARPS
-#define ASSE_OWN_CONS_WARPS 12
+#define ASSE_OWN_CONS_WARPS 8
 #endif
 #ifndef ASSE_OWN_CHECK
 #define ASSE_OWN_CHECK 0
@@ -40,27 +40,40 @@ namespace asse {
 #ifndef ASSE_OWN_NGR
 #define ASSE_OWN_NGR 2
 #endif
-#ifndef ASSE_OWN_U
-#define ASSE_OWN_U 1
+#ifndef ASSE_OWN_NOTPR
+#define ASSE_OWN_NOTPR 1
 #endif
-// warps (measured at C5 on B200, tools/gpu_own_sweep2.sh; the drain is the longer phase):
-// 16 binning + 8 draining warps 0.98 ms, + 10 1.07, + 12 0.94, + 14 0.95 (64 registers)
+#ifndef ASSE_OWN_X2
+#define ASSE_OWN_X2 1
+#endif
+#ifndef ASSE_OWN_U
+#define ASSE_OWN_U 2
+#endif
+// warps (measured at C5 on B200, tools/gpu_own_sweep2.sh, gpu_own13.sh): with runtime geometry
+// 16 binning + 8 / 10 / 12 / 14 draining warps 0.98 / 1.07 / 0.94 / 0.95 ms; with the C3
+// geometry folded (cheaper drain) 6 / 8 / 10 / 12 warps 0.95 / 0.82 / 0.86 / 0.84 ms, 8 warps
+// with two 16-B groups in flight per ring 0.81 ms
 constexpr int kOwnBinWarps = ASSE_OWN_BIN_WARPS;           // binning + shipping warps
 constexpr int kOwnConsWarps = ASSE_OWN_CONS_WARPS;         // queue-draining warps, two groups (round parity)
 constexpr int kOwnConsWarp0 = kOwnBinWarps;
 constexpr int kOwnTmaWarp = kOwnConsWarp0 + kOwnConsWarps;
 constexpr int kOwnSigWarp = kOwnTmaWarp + 1;
 constexpr int kOwnThreads = 32 * (kOwnSigWarp + 1);
-constexpr int kOwnRing = 2;                                // packet-tile ring stages
-constexpr int kOwnCap = 30;                                // staged entries per (owner, round) in a CTA
-constexpr int kOwnStride = 30;                             // entries (8 B) between bins: 240 B, 16-B aligned;
-                                                           // bin o starts at bank 28o mod 32
+constexpr int kOwnRing = 2;                                // packet-tile ring stages per tile of a round
+constexpr int kOwnCap = 30;                                // staged entries per (owner, round) in a CTA; also
+                                                           // the bin stride (240 B, 16-B aligned; bin o
+                                                           // starts at bank 28o mod 32)
+// CTAs that own no slice have its shared memory free: they take NOTPR tiles per round
+// (bins of NOTPR * kOwnCap entries), which takes binning work off the owners' SMs, whose
+// draining warps compete with their binning warps, and shortens the run by rounds
+constexpr uint32_t kOwnNoTpr = ASSE_OWN_NOTPR;
+constexpr int kOwnRingMax = kOwnRing * kOwnNoTpr;
 constexpr uint32_t kOwnNB = ASSE_OWN_NB;                   // queue buffers (rounds) in flight (C5: 4 -> 0.952 ms,
                                                            // 6 0.942, 8 0.927; tools/gpu_own_sweep4.sh)
 constexpr uint32_t kOwnNGR = ASSE_OWN_NGR;                 // drain groups (round t -> group t mod NGR)
 static_assert(kOwnNB % kOwnNGR == 0 && kOwnConsWarps % kOwnNGR == 0, "drain groups");
-constexpr uint32_t kOwnQCap = 2048;                        // ring entries per (buffer, owner, group)
-                                                           // >= ceil(G / QG) * kOwnCap
+constexpr uint32_t kOwnQCap = 2048;                        // ring entries per (buffer, owner, group) >= the
+                                                           // producer group's bins (host-checked)
 constexpr uint32_t kOwnMaxOwners = 128;                   // F * NGRP: a power of two <= the SMs
 constexpr uint32_t kOwnMinTilesPerCta = 8;                 // below: k_scan is used
 
@@ -76,10 +89,19 @@ struct OwnScanParams {
   unsigned long long* prof;  // optional per-CTA phase cycle counters [G][16] (tools; may be null)
 };
 
-// slice words of one owner: r rows x 2^c ATVs x WG words
-__host__ __device__ constexpr size_t own_smem_bytes(uint32_t O, uint32_t slice_words, uint32_t tile_bytes) {
-  return (size_t)kOwnRing * tile_bytes + 2 * (size_t)O * kOwnStride * 8 + 2 * (((size_t)O * 4 + 15) & ~(size_t)15) +
+// dynamic shared memory: owners [ring 2 tiles][staging 2 x O x CAP][counts][slice];
+// non-owners [ring 2 NOTPR tiles][staging 2 x O x NOTPR CAP][counts]
+__host__ __device__ constexpr size_t own_smem_owner(uint32_t O, uint32_t slice_words, uint32_t tile_bytes) {
+  return (size_t)kOwnRing * tile_bytes + 2 * (size_t)O * kOwnCap * 8 + 2 * (((size_t)O * 4 + 15) & ~(size_t)15) +
          16 + (size_t)slice_words * 4;
+}
+__host__ __device__ constexpr size_t own_smem_nonowner(uint32_t O, uint32_t tile_bytes) {
+  return (size_t)kOwnRingMax * tile_bytes + 2 * (size_t)O * kOwnCap * kOwnNoTpr * 8 +
+         2 * (((size_t)O * 4 + 15) & ~(size_t)15) + 16;
+}
+__host__ __device__ constexpr size_t own_smem_bytes(uint32_t O, uint32_t slice_words, uint32_t tile_bytes) {
+  return own_smem_owner(O, slice_words, tile_bytes) > own_smem_nonowner(O, tile_bytes)
+             ? own_smem_owner(O, slice_words, tile_bytes) : own_smem_nonowner(O, tile_bytes);
 }
 
 #ifndef ASSE_OWN_SPIN
@@ -168,7 +190,7 @@ __device__ __forceinline__ void own_apply(const OwnScanParams& op, uint32_t* sbm
 // global bitmap (k_scan's REDs). Called by whole warps; lanes with !valid do nothing.
 template <int CB, bool MP, class Geo>
 __device__ __forceinline__ void own_bin_two(const OwnScanParams& op, const uint4 v, bool valid, uint32_t stg_s,
-                                            uint32_t scount_s, uint32_t scount_dummy) {
+                                            uint32_t scount_s, uint32_t scount_dummy, uint32_t cap) {
   const ScanParams& p = op.sp;
   const uint32_t h0 = MP ? walk_mod_p(p.A, v.x) : (uint32_t)p.A * v.x;   // f(aip)
   const uint32_t h1 = MP ? walk_mod_p(p.A, v.z) : (uint32_t)p.A * v.z;
@@ -180,11 +202,9 @@ __device__ __forceinline__ void own_bin_two(const OwnScanParams& op, const uint4
   const uint32_t o1 = ((h1 & fm) << Geo::lg_ngrp(op)) | (i1 >> gs);
   const uint32_t pos0 = atoms_inc(valid ? scount_s + 4u * o0 : scount_dummy);
   const uint32_t pos1 = atoms_inc(valid ? scount_s + 4u * o1 : scount_dummy);
-  const bool ok0 = pos0 < (uint32_t)kOwnCap, ok1 = pos1 < (uint32_t)kOwnCap;
-  sts64_if(valid && ok0, stg_s + 8u * (o0 * kOwnStride + pos0), (h0 & ~fm) | ((i0 >> 5) & wgm),
-           1u << touch_bit<CB>(i0));
-  sts64_if(valid && ok1, stg_s + 8u * (o1 * kOwnStride + pos1), (h1 & ~fm) | ((i1 >> 5) & wgm),
-           1u << touch_bit<CB>(i1));
+  const bool ok0 = pos0 < cap, ok1 = pos1 < cap;
+  sts64_if(valid && ok0, stg_s + 8u * (o0 * cap + pos0), (h0 & ~fm) | ((i0 >> 5) & wgm), 1u << touch_bit<CB>(i0));
+  sts64_if(valid && ok1, stg_s + 8u * (o1 * cap + pos1), (h1 & ~fm) | ((i1 >> 5) & wgm), 1u << touch_bit<CB>(i1));
   const bool ov0 = valid && !ok0, ov1 = valid && !ok1;
   if (__any_sync(0xffffffffu, ov0 || ov1)) {
     if (ov0) scan_pair<CB, MP>(p, v.x, v.y);
@@ -199,33 +219,38 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int kSig = 2 * kOwnNB;
   static_assert(kSig > kOwnNB + 1, "signal barrier ring");
-  __shared__ __align__(8) uint64_t full[kOwnRing], empty[kOwnRing], sigbar[kSig];
+  __shared__ __align__(8) uint64_t full[kOwnRingMax], empty[kOwnRingMax], sigbar[kSig];
   __shared__ uint32_t slast[kOwnNB][kBinQG];     // drain: end of the last drained round per buffer/ring
   const uint32_t G = gridDim.x, me = blockIdx.x, O = op.O;
   const uint32_t Op = (O + 3u) & ~3u;
+  const bool owner = me < O;
+  const uint32_t tpr = owner ? 1u : kOwnNoTpr;   // tiles per round
+  const uint32_t nst = kOwnRing * tpr;           // ring stages
+  const uint32_t cap = kOwnCap * tpr;            // bin capacity and stride (entries)
+  const uint32_t T = O + kOwnNoTpr * (G - O);    // tiles per round, all CTAs
+  const uint32_t tbase = owner ? me : O + kOwnNoTpr * (me - O);   // this CTA's first tile of a round
   uint8_t* ring = smem;
-  uint2* stg = reinterpret_cast<uint2*>(smem + (size_t)kOwnRing * kTileBytes);         // [2][O][STRIDE]
-  uint32_t* scount = reinterpret_cast<uint32_t*>(stg + 2 * (size_t)O * kOwnStride);    // [2][Op]
-  uint32_t* sbm = scount + 2 * Op + 4;           // 4 spare words: dummy bin counter
+  uint2* stg = reinterpret_cast<uint2*>(smem + (size_t)nst * kTileBytes);             // [2][O][cap]
+  uint32_t* scount = reinterpret_cast<uint32_t*>(stg + 2 * (size_t)O * cap);          // [2][Op]
+  uint32_t* sbm = scount + 2 * Op + 4;           // 4 spare words: dummy bin counter (owners: the slice)
   const uint32_t slice_words = (uint32_t)op.sp.r << (op.sp.c + op.lg_wg);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint32_t head = (((uintptr_t)pk) & 15u) ? 1u : 0u;
   const uint64_t nbody = (n > head) ? n - head : 0;
   const uint64_t body_bytes = (nbody >> 1) * 16u;
   const uint64_t n_tiles = (body_bytes + kTileBytes - 1) / kTileBytes;
-  const uint32_t R = (uint32_t)((n_tiles + G - 1) / G);        // rounds; tile of CTA b in round t: t*G + b
+  const uint32_t R = (uint32_t)((n_tiles + T - 1) / T);        // rounds; tiles of CTA b in round t: t*T + tbase + k
   uint32_t* prod_done = op.sync;
   uint32_t* cons_done = op.sync + kOwnNB * kBinPad;
   constexpr int kBinT = 32 * kOwnBinWarps;                    // named barrier 1
   constexpr int kGroupThreads = 32 * (kOwnConsWarps / kOwnNGR);   // named barriers 2 .. 1 + NGR
   constexpr int kComputeThreads = 32 * (kOwnBinWarps + kOwnConsWarps);   // named barrier 8
-  const bool owner = me < O;
 
   if (owner)
     for (uint32_t q = threadIdx.x; q < slice_words; q += blockDim.x) sbm[q] = 0;
   for (uint32_t q = threadIdx.x; q < 2 * Op; q += blockDim.x) scount[q] = 0;
   if (threadIdx.x == 0) {
-    for (int st = 0; st < kOwnRing; ++st) {
+    for (int st = 0; st < kOwnRingMax; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], kOwnBinWarps);
     }
@@ -250,17 +275,18 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       uint32_t i = 0;
-      for (uint32_t t = 0; t < R; ++t) {
-        const uint64_t tile = (uint64_t)t * G + me;
-        if (tile >= n_tiles) break;
-        const uint32_t st = i % kOwnRing;
-        if (i >= (uint32_t)kOwnRing) mbar_wait_suspend(&empty[st], ((i / kOwnRing) - 1) & 1u);
-        const uint64_t off = tile * (uint64_t)kTileBytes;
-        const uint32_t bytes = (uint32_t)umin64(kTileBytes, body_bytes - off);
-        mbar_expect_tx(&full[st], bytes);
-        bulk_g2s(ring + (size_t)st * kTileBytes, body + off, bytes, &full[st], pol);
-        ++i;
-      }
+      for (uint32_t t = 0; t < R; ++t)
+        for (uint32_t k = 0; k < tpr; ++k) {
+          const uint64_t tile = (uint64_t)t * T + tbase + k;
+          if (tile >= n_tiles) break;
+          const uint32_t st = i % nst;
+          if (i >= nst) mbar_wait_suspend(&empty[st], ((i / nst) - 1) & 1u);
+          const uint64_t off = tile * (uint64_t)kTileBytes;
+          const uint32_t bytes = (uint32_t)umin64(kTileBytes, body_bytes - off);
+          mbar_expect_tx(&full[st], bytes);
+          bulk_g2s(ring + (size_t)st * kTileBytes, body + off, bytes, &full[st], pol);
+          ++i;
+        }
     }
     return;
   }
@@ -281,37 +307,47 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       uint32_t cnt = 0, off = 0;
       if (t >= 1 && my_o < O) {
         // whole 16-B groups: pad the bin with a "no entry" entry up to an even count
-        const uint32_t c = min(scount[sf * Op + my_o], (uint32_t)kOwnCap);
+        const uint32_t c = min(scount[sf * Op + my_o], cap);
         cnt = (c + 1u) & ~1u;
-        if (c & 1u) stg[((size_t)sf * O + my_o) * kOwnStride + c] = make_uint2(0u, 0u);   // mask 0: no entry
+        if (c & 1u) stg[((size_t)sf * O + my_o) * cap + c] = make_uint2(0u, 0u);   // mask 0: no entry
         if (cnt) off = atomicAdd(op.qcnt + (((size_t)bf * O + my_o) * kBinQG + (me % kBinQG)) * kBinPad, cnt);
       }
       c1 = clock64(); pc[1] += c1 - c0; c0 = c1;
       uint32_t seen = 0;
       const uint32_t need = O * (t / kOwnNB);    // owners that drained round t - NB
       if (tid == 0 && t >= (uint32_t)kOwnNB && t < R) seen = ld_relaxed_gpu(cons_done + (t % kOwnNB) * kBinPad);
-      if (t < R) {
-        const uint64_t tile = (uint64_t)t * G + me;
-        if (tile < n_tiles) {
-          const uint32_t st = i % kOwnRing;
-          mbar_wait(&full[st], (i / kOwnRing) & 1u);
-          const uint32_t n4 = (uint32_t)umin64(kTileBytes, body_bytes - tile * (uint64_t)kTileBytes) >> 4;
-          const uint4* tp = reinterpret_cast<const uint4*>(ring + (size_t)st * kTileBytes);
-          const uint32_t stg_s = smem_u32(stg + (size_t)sb * O * kOwnStride), scount_s = smem_u32(scount + sb * Op);
-          const uint32_t dummy_s = smem_u32(scount + 2 * Op);
-          for (uint32_t q0 = tid - lane; q0 < n4; q0 += kBinT) {   // warp-uniform trip count
-            const uint32_t q = q0 + lane;
-            const bool valid = q < n4;
-            own_bin_two<CB, MP, Geo>(op, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s, dummy_s);
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[st]);
-          ++i;
+      for (uint32_t k = 0; t < R && k < tpr; ++k) {
+        const uint64_t tile = (uint64_t)t * T + tbase + k;
+        if (tile >= n_tiles) break;
+        const uint32_t st = i % nst;
+        mbar_wait(&full[st], (i / nst) & 1u);
+        const uint32_t n4 = (uint32_t)umin64(kTileBytes, body_bytes - tile * (uint64_t)kTileBytes) >> 4;
+        const uint4* tp = reinterpret_cast<const uint4*>(ring + (size_t)st * kTileBytes);
+        const uint32_t stg_s = smem_u32(stg + (size_t)sb * O * cap), scount_s = smem_u32(scount + sb * Op);
+        const uint32_t dummy_s = smem_u32(scount + 2 * Op);
+#if ASSE_OWN_X2
+        for (uint32_t q0 = tid - lane; q0 < n4; q0 += 2 * kBinT) {   // warp-uniform trip count
+          const uint32_t q = q0 + lane, q1 = q + kBinT;
+          const bool valid = q < n4, valid1 = q1 < n4;
+          const uint4 v0 = valid ? tp[q] : make_uint4(0, 0, 0, 0);
+          const uint4 v1 = valid1 ? tp[q1] : make_uint4(0, 0, 0, 0);
+          own_bin_two<CB, MP, Geo>(op, v0, valid, stg_s, scount_s, dummy_s, cap);
+          own_bin_two<CB, MP, Geo>(op, v1, valid1, stg_s, scount_s, dummy_s, cap);
         }
+#else
+        for (uint32_t q0 = tid - lane; q0 < n4; q0 += kBinT) {   // warp-uniform trip count
+          const uint32_t q = q0 + lane;
+          const bool valid = q < n4;
+          own_bin_two<CB, MP, Geo>(op, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s, dummy_s, cap);
+        }
+#endif
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        ++i;
       }
       c1 = clock64(); pc[0] += c1 - c0; c0 = c1;
       if (t >= 1) {
-        const uint2* stg_f = stg + (size_t)sf * O * kOwnStride;
+        const uint2* stg_f = stg + (size_t)sf * O * cap;
         uint2* qb = op.queue + ((size_t)bf * O * kBinQG + (me % kBinQG)) * kOwnQCap;
         // two owners per step (one per half-warp), 16 B (two entries) per lane
         const uint32_t hl = lane & 15u, hw = lane >> 4;
@@ -325,7 +361,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
           of[k] = __shfl_sync(0xffffffffu, off, 2 * k + hw);
           const uint32_t ow = warp + kOwnBinWarps * (2 * k + hw);
           if (2 * hl < c2[k]) {
-            const uint32_t a = smem_u32(stg_f + (size_t)ow * kOwnStride) + 16u * hl;
+            const uint32_t a = smem_u32(stg_f + (size_t)ow * cap) + 16u * hl;
             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                          : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w) : "r"(a));
           }
@@ -336,6 +372,21 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
           if (2 * hl < c2[k]) {
             uint4* dst = reinterpret_cast<uint4*>(qb + (size_t)ow * kBinQG * kOwnQCap);
             dst[((of[k] >> 1) + hl) & (kOwnQCap / 2 - 1)] = v[k];
+          }
+        }
+        // bins longer than 32 entries (non-owner CTAs): 16-B groups 16.. of those owners
+        if (cap > 32u) {
+#pragma unroll
+          for (int k = 0; k < NS; ++k) {
+            const uint32_t ow = warp + kOwnBinWarps * (2 * k + hw);
+            for (uint32_t j = hl + 16u; 2u * j < c2[k]; j += 16u) {
+              uint4 x;
+              asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                           : "r"(smem_u32(stg_f + (size_t)ow * cap) + 16u * j));
+              uint4* dst = reinterpret_cast<uint4*>(qb + (size_t)ow * kBinQG * kOwnQCap);
+              dst[((of[k] >> 1) + j) & (kOwnQCap / 2 - 1)] = x;
+            }
           }
         }
         if (my_o < O) scount[sf * Op + my_o] = 0;
