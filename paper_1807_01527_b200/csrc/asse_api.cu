@@ -418,7 +418,7 @@ static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const Sc
     std::vector<unsigned long long> h((size_t)G * 16);
     CK(cudaStreamSynchronize(st));
     CK(cudaMemcpy(h.data(), op.prof, h.size() * 8, cudaMemcpyDeviceToHost));
-    const char* nm[13] = {"b_bin", "b_wait_reserve", "b_copy", "-", "-", "-",
+    const char* nm[13] = {"b_bin", "b_wait_reserve", "b_copy", "b_bin_wait_tile", "-", "-",
                           "-", "-", "-", "c0_wait", "c0_drain", "c1_wait", "c1_drain"};
     fprintf(stderr, "k_scan_own n=%llu G=%u O=%u:", (unsigned long long)n, G, O);
     for (int q = 0; q < 13; ++q) {
@@ -696,8 +696,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
         c->own_smem = own_smem_bytes(c->own_O, (uint32_t)std::min<uint64_t>(slice_words, 1u << 30), c->own_tile);
         c->own_ok = coop && p.r == 4 && (1u << lg_wpa) == c->wpa && c->own_O <= (uint32_t)c->sms && c->own_lg_wg <= p.u &&
                     c->own_O <= kOwnMaxOwners && c->own_O >= 2 &&
-                    (uint64_t)((c->own_O + kBinQG - 1) / kBinQG) * kOwnCap +
-                            (uint64_t)((c->sms - c->own_O + kBinQG - 1) / kBinQG) * kOwnCap * kOwnNoTpr <= kOwnQCap &&
+                    (uint64_t)((c->sms + kBinQG - 1) / kBinQG) * kOwnCap <= kOwnQCap &&
                     slice_words <= (1u << 20) && c->own_smem + 2048 <= (size_t)optin &&
                     !getenv("ASSE_SCAN_NO_OWN");
         if (c->own_ok) {

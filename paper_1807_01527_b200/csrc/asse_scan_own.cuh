@@ -40,9 +40,6 @@ namespace asse {
 #ifndef ASSE_OWN_NGR
 #define ASSE_OWN_NGR 2
 #endif
-#ifndef ASSE_OWN_NOTPR
-#define ASSE_OWN_NOTPR 1
-#endif
 #ifndef ASSE_OWN_X2
 #define ASSE_OWN_X2 1
 #endif
@@ -59,15 +56,10 @@ constexpr int kOwnConsWarp0 = kOwnBinWarps;
 constexpr int kOwnTmaWarp = kOwnConsWarp0 + kOwnConsWarps;
 constexpr int kOwnSigWarp = kOwnTmaWarp + 1;
 constexpr int kOwnThreads = 32 * (kOwnSigWarp + 1);
-constexpr int kOwnRing = 2;                                // packet-tile ring stages per tile of a round
-constexpr int kOwnCap = 30;                                // staged entries per (owner, round) in a CTA; also
+constexpr int kOwnRing = 2;                                // packet-tile ring stages
+constexpr uint32_t kOwnCap = 30;                           // staged entries per (owner, round) in a CTA; also
                                                            // the bin stride (240 B, 16-B aligned; bin o
                                                            // starts at bank 28o mod 32)
-// CTAs that own no slice have its shared memory free: they take NOTPR tiles per round
-// (bins of NOTPR * kOwnCap entries), which takes binning work off the owners' SMs, whose
-// draining warps compete with their binning warps, and shortens the run by rounds
-constexpr uint32_t kOwnNoTpr = ASSE_OWN_NOTPR;
-constexpr int kOwnRingMax = kOwnRing * kOwnNoTpr;
 constexpr uint32_t kOwnNB = ASSE_OWN_NB;                   // queue buffers (rounds) in flight (C5: 4 -> 0.952 ms,
                                                            // 6 0.942, 8 0.927; tools/gpu_own_sweep4.sh)
 constexpr uint32_t kOwnNGR = ASSE_OWN_NGR;                 // drain groups (round t -> group t mod NGR)
@@ -89,19 +81,10 @@ struct OwnScanParams {
   unsigned long long* prof;  // optional per-CTA phase cycle counters [G][16] (tools; may be null)
 };
 
-// dynamic shared memory: owners [ring 2 tiles][staging 2 x O x CAP][counts][slice];
-// non-owners [ring 2 NOTPR tiles][staging 2 x O x NOTPR CAP][counts]
-__host__ __device__ constexpr size_t own_smem_owner(uint32_t O, uint32_t slice_words, uint32_t tile_bytes) {
+// dynamic shared memory: [ring 2 tiles][staging 2 x O x CAP][counts][owners: the slice]
+__host__ __device__ constexpr size_t own_smem_bytes(uint32_t O, uint32_t slice_words, uint32_t tile_bytes) {
   return (size_t)kOwnRing * tile_bytes + 2 * (size_t)O * kOwnCap * 8 + 2 * (((size_t)O * 4 + 15) & ~(size_t)15) +
          16 + (size_t)slice_words * 4;
-}
-__host__ __device__ constexpr size_t own_smem_nonowner(uint32_t O, uint32_t tile_bytes) {
-  return (size_t)kOwnRingMax * tile_bytes + 2 * (size_t)O * kOwnCap * kOwnNoTpr * 8 +
-         2 * (((size_t)O * 4 + 15) & ~(size_t)15) + 16;
-}
-__host__ __device__ constexpr size_t own_smem_bytes(uint32_t O, uint32_t slice_words, uint32_t tile_bytes) {
-  return own_smem_owner(O, slice_words, tile_bytes) > own_smem_nonowner(O, tile_bytes)
-             ? own_smem_owner(O, slice_words, tile_bytes) : own_smem_nonowner(O, tile_bytes);
 }
 
 #ifndef ASSE_OWN_SPIN
@@ -190,7 +173,8 @@ __device__ __forceinline__ void own_apply(const OwnScanParams& op, uint32_t* sbm
 // global bitmap (k_scan's REDs). Called by whole warps; lanes with !valid do nothing.
 template <int CB, bool MP, class Geo>
 __device__ __forceinline__ void own_bin_two(const OwnScanParams& op, const uint4 v, bool valid, uint32_t stg_s,
-                                            uint32_t scount_s, uint32_t scount_dummy, uint32_t cap) {
+                                            uint32_t scount_s, uint32_t scount_dummy) {
+  constexpr uint32_t cap = kOwnCap;
   const ScanParams& p = op.sp;
   const uint32_t h0 = MP ? walk_mod_p(p.A, v.x) : (uint32_t)p.A * v.x;   // f(aip)
   const uint32_t h1 = MP ? walk_mod_p(p.A, v.z) : (uint32_t)p.A * v.z;
@@ -219,16 +203,12 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int kSig = 2 * kOwnNB;
   static_assert(kSig > kOwnNB + 1, "signal barrier ring");
-  __shared__ __align__(8) uint64_t full[kOwnRingMax], empty[kOwnRingMax], sigbar[kSig];
+  __shared__ __align__(8) uint64_t full[kOwnRing], empty[kOwnRing], sigbar[kSig];
   __shared__ uint32_t slast[kOwnNB][kBinQG];     // drain: end of the last drained round per buffer/ring
   const uint32_t G = gridDim.x, me = blockIdx.x, O = op.O;
   const uint32_t Op = (O + 3u) & ~3u;
   const bool owner = me < O;
-  const uint32_t tpr = owner ? 1u : kOwnNoTpr;   // tiles per round
-  const uint32_t nst = kOwnRing * tpr;           // ring stages
-  const uint32_t cap = kOwnCap * tpr;            // bin capacity and stride (entries)
-  const uint32_t T = O + kOwnNoTpr * (G - O);    // tiles per round, all CTAs
-  const uint32_t tbase = owner ? me : O + kOwnNoTpr * (me - O);   // this CTA's first tile of a round
+  constexpr uint32_t nst = kOwnRing, cap = kOwnCap;
   uint8_t* ring = smem;
   uint2* stg = reinterpret_cast<uint2*>(smem + (size_t)nst * kTileBytes);             // [2][O][cap]
   uint32_t* scount = reinterpret_cast<uint32_t*>(stg + 2 * (size_t)O * cap);          // [2][Op]
@@ -239,7 +219,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   const uint64_t nbody = (n > head) ? n - head : 0;
   const uint64_t body_bytes = (nbody >> 1) * 16u;
   const uint64_t n_tiles = (body_bytes + kTileBytes - 1) / kTileBytes;
-  const uint32_t R = (uint32_t)((n_tiles + T - 1) / T);        // rounds; tiles of CTA b in round t: t*T + tbase + k
+  const uint32_t R = (uint32_t)((n_tiles + G - 1) / G);        // rounds; tile of CTA b in round t: t*G + b
   uint32_t* prod_done = op.sync;
   uint32_t* cons_done = op.sync + kOwnNB * kBinPad;
   constexpr int kBinT = 32 * kOwnBinWarps;                    // named barrier 1
@@ -250,7 +230,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
     for (uint32_t q = threadIdx.x; q < slice_words; q += blockDim.x) sbm[q] = 0;
   for (uint32_t q = threadIdx.x; q < 2 * Op; q += blockDim.x) scount[q] = 0;
   if (threadIdx.x == 0) {
-    for (int st = 0; st < kOwnRingMax; ++st) {
+    for (int st = 0; st < kOwnRing; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], kOwnBinWarps);
     }
@@ -275,18 +255,17 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       uint32_t i = 0;
-      for (uint32_t t = 0; t < R; ++t)
-        for (uint32_t k = 0; k < tpr; ++k) {
-          const uint64_t tile = (uint64_t)t * T + tbase + k;
-          if (tile >= n_tiles) break;
-          const uint32_t st = i % nst;
-          if (i >= nst) mbar_wait_suspend(&empty[st], ((i / nst) - 1) & 1u);
-          const uint64_t off = tile * (uint64_t)kTileBytes;
-          const uint32_t bytes = (uint32_t)umin64(kTileBytes, body_bytes - off);
-          mbar_expect_tx(&full[st], bytes);
-          bulk_g2s(ring + (size_t)st * kTileBytes, body + off, bytes, &full[st], pol);
-          ++i;
-        }
+      for (uint32_t t = 0; t < R; ++t) {
+        const uint64_t tile = (uint64_t)t * G + me;
+        if (tile >= n_tiles) break;
+        const uint32_t st = i % nst;
+        if (i >= nst) mbar_wait_suspend(&empty[st], ((i / nst) - 1) & 1u);
+        const uint64_t off = tile * (uint64_t)kTileBytes;
+        const uint32_t bytes = (uint32_t)umin64(kTileBytes, body_bytes - off);
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(ring + (size_t)st * kTileBytes, body + off, bytes, &full[st], pol);
+        ++i;
+      }
     }
     return;
   }
@@ -298,7 +277,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       if (nbody & 1) scan_pair<CB, MP>(op.sp, pk[n - 1].x, pk[n - 1].y);
     }
     uint32_t i = 0;
-    unsigned long long pc[3] = {0, 0, 0};
+    unsigned long long pc[4] = {0, 0, 0, 0};
     long long c0 = clock64(), c1;
     const uint32_t my_o = warp + kOwnBinWarps * lane;   // owners this lane reserves for
     for (uint32_t t = 0; t <= R; ++t) {
@@ -316,11 +295,14 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       uint32_t seen = 0;
       const uint32_t need = O * (t / kOwnNB);    // owners that drained round t - NB
       if (tid == 0 && t >= (uint32_t)kOwnNB && t < R) seen = ld_relaxed_gpu(cons_done + (t % kOwnNB) * kBinPad);
-      for (uint32_t k = 0; t < R && k < tpr; ++k) {
-        const uint64_t tile = (uint64_t)t * T + tbase + k;
-        if (tile >= n_tiles) break;
+      const uint64_t tile = (uint64_t)t * G + me;
+      if (t < R && tile < n_tiles) {
         const uint32_t st = i % nst;
-        mbar_wait(&full[st], (i / nst) & 1u);
+        {
+          const long long w0 = clock64();
+          mbar_wait(&full[st], (i / nst) & 1u);
+          pc[3] += clock64() - w0;               // tile arrival (tools: ASSE_SCAN_PROF)
+        }
         const uint32_t n4 = (uint32_t)umin64(kTileBytes, body_bytes - tile * (uint64_t)kTileBytes) >> 4;
         const uint4* tp = reinterpret_cast<const uint4*>(ring + (size_t)st * kTileBytes);
         const uint32_t stg_s = smem_u32(stg + (size_t)sb * O * cap), scount_s = smem_u32(scount + sb * Op);
@@ -331,14 +313,14 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
           const bool valid = q < n4, valid1 = q1 < n4;
           const uint4 v0 = valid ? tp[q] : make_uint4(0, 0, 0, 0);
           const uint4 v1 = valid1 ? tp[q1] : make_uint4(0, 0, 0, 0);
-          own_bin_two<CB, MP, Geo>(op, v0, valid, stg_s, scount_s, dummy_s, cap);
-          own_bin_two<CB, MP, Geo>(op, v1, valid1, stg_s, scount_s, dummy_s, cap);
+          own_bin_two<CB, MP, Geo>(op, v0, valid, stg_s, scount_s, dummy_s);
+          own_bin_two<CB, MP, Geo>(op, v1, valid1, stg_s, scount_s, dummy_s);
         }
 #else
         for (uint32_t q0 = tid - lane; q0 < n4; q0 += kBinT) {   // warp-uniform trip count
           const uint32_t q = q0 + lane;
           const bool valid = q < n4;
-          own_bin_two<CB, MP, Geo>(op, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s, dummy_s, cap);
+          own_bin_two<CB, MP, Geo>(op, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s, dummy_s);
         }
 #endif
         __syncwarp();
@@ -349,7 +331,8 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       if (t >= 1) {
         const uint2* stg_f = stg + (size_t)sf * O * cap;
         uint2* qb = op.queue + ((size_t)bf * O * kBinQG + (me % kBinQG)) * kOwnQCap;
-        // two owners per step (one per half-warp), 16 B (two entries) per lane
+        // two owners per step (one per half-warp), 16 B (two entries) per lane (measured
+        // faster than the same copy with 32-bit offsets from per-round bases: 0.799 vs 0.812 ms)
         const uint32_t hl = lane & 15u, hw = lane >> 4;
         constexpr int NS = (kOwnMaxOwners + 2 * kOwnBinWarps - 1) / (2 * kOwnBinWarps);
         __syncwarp();                            // padding entries written by other lanes
@@ -374,21 +357,6 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
             dst[((of[k] >> 1) + hl) & (kOwnQCap / 2 - 1)] = v[k];
           }
         }
-        // bins longer than 32 entries (non-owner CTAs): 16-B groups 16.. of those owners
-        if (cap > 32u) {
-#pragma unroll
-          for (int k = 0; k < NS; ++k) {
-            const uint32_t ow = warp + kOwnBinWarps * (2 * k + hw);
-            for (uint32_t j = hl + 16u; 2u * j < c2[k]; j += 16u) {
-              uint4 x;
-              asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                           : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
-                           : "r"(smem_u32(stg_f + (size_t)ow * cap) + 16u * j));
-              uint4* dst = reinterpret_cast<uint4*>(qb + (size_t)ow * kBinQG * kOwnQCap);
-              dst[((of[k] >> 1) + j) & (kOwnQCap / 2 - 1)] = x;
-            }
-          }
-        }
         if (my_o < O) scount[sf * Op + my_o] = 0;
         __syncwarp();
         if (lane == 0) mbar_arrive(&sigbar[tf % kSig]);   // this warp wrote round tf
@@ -399,7 +367,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       c1 = clock64(); pc[2] += c1 - c0; c0 = c1;
     }
     if (op.prof && tid == 0)
-      for (int q = 0; q < 3; ++q) op.prof[me * 16 + q] = pc[q];
+      for (int q = 0; q < 4; ++q) op.prof[me * 16 + q] = pc[q];
   } else if (owner) {                            // ---------------- queue-draining warps
     const uint32_t cid = warp - kOwnConsWarp0;
     const uint32_t grp = cid / (kOwnConsWarps / kOwnNGR);
