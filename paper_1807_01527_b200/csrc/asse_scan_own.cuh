@@ -31,9 +31,6 @@ namespace asse {
 #ifndef ASSE_OWN_CONS_WARPS
 #define ASSE_OWN_CONS_WARPS 8
 #endif
-#ifndef ASSE_OWN_CHECK
-#define ASSE_OWN_CHECK 0
-#endif
 #ifndef ASSE_OWN_NB
 #define ASSE_OWN_NB 8
 #endif
@@ -87,17 +84,10 @@ __host__ __device__ constexpr size_t own_smem_bytes(uint32_t O, uint32_t slice_w
          16 + (size_t)slice_words * 4;
 }
 
-#ifndef ASSE_OWN_SPIN
-#define ASSE_OWN_SPIN 1
-#endif
-#ifndef ASSE_OWN_POLL_NS
-#define ASSE_OWN_POLL_NS 1
-#endif
 // mbarrier wait for warps off the critical path: the hardware suspends the thread until
 // the phase completes or the hint (ns) expires, so the wait costs no issue slots (a
 // nanosleep poll loop cost ~8 % of the kernel's instructions, ncu r01g)
 __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t phase) {
-#if ASSE_OWN_SPIN
   uint32_t done = 0;
   while (!done) {
     asm volatile(
@@ -106,9 +96,6 @@ __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t phase)
         " selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done) : "r"(smem_u32(bar)), "r"(phase), "r"(1000000u) : "memory");
   }
-#else
-  mbar_wait_sleep(bar, phase, 1000);
-#endif
 }
 
 __device__ __forceinline__ void sts64_if(bool pred, uint32_t addr, uint32_t a, uint32_t b) {
@@ -157,12 +144,7 @@ __device__ __forceinline__ void own_apply(const OwnScanParams& op, uint32_t* sbm
   for (int y = 0; y < 4; ++y) {
     const uint32_t x = (uint32_t)(D >> Geo::shift(op, y)) & Geo::cmask(op);
     const uint32_t w = (((((uint32_t)y << Geo::c(op)) | x) << Geo::lg_wg(op)) | sub);
-#if ASSE_OWN_CHECK
-    uint32_t* a = sbm + w;
-    if (!(*reinterpret_cast<volatile uint32_t*>(a) & m)) atomicOr(a, m);
-#else
     atomicOr(sbm + w, m);
-#endif
   }
 }
 
@@ -362,7 +344,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         if (lane == 0) mbar_arrive(&sigbar[tf % kSig]);   // this warp wrote round tf
       }
       if (tid == 0 && t >= (uint32_t)kOwnNB && t < R && seen < need)
-        spin_until_geq(cons_done + (t % kOwnNB) * kBinPad, need, 128 * ASSE_OWN_POLL_NS);   // round t-NB drained
+        spin_until_geq(cons_done + (t % kOwnNB) * kBinPad, need, 128);   // round t-NB drained
       named_bar(1, kBinT);                       // bins of round t final; staging sf and counts reusable
       c1 = clock64(); pc[2] += c1 - c0; c0 = c1;
     }
@@ -377,7 +359,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
     long long c0 = clock64(), c1;
     for (uint32_t t = grp; t < R; t += kOwnNGR) {
       const uint32_t b = t % kOwnNB;
-      if (gtid == 0) spin_until_geq(prod_done + b * kBinPad, G * (t / kOwnNB + 1), 300 * ASSE_OWN_POLL_NS);
+      if (gtid == 0) spin_until_geq(prod_done + b * kBinPad, G * (t / kOwnNB + 1), 300);
       named_bar(2 + grp, kGroupThreads);
       c1 = clock64(); cwait += c1 - c0; c0 = c1;
       // the round's entries: QG ranges [start, end) of the owner's rings of buffer b; start =
