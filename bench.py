@@ -342,6 +342,11 @@ def main():
         for q in range(2):
             host[q].copy_(bufs[q])
         torch.cuda.synchronize()
+        # untimed warm-up of the host path (its staging buffers are allocated on first use)
+        for t in range(min(args.warmup, 2)):
+            ctx.scan_slice_host(host[t % 2])
+            ctx.end_slice(0)
+        torch.cuda.synchronize()
         d2h = 0
         barrier()
         torch.cuda.synchronize()
