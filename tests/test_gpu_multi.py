@@ -34,6 +34,14 @@ def test_virtual_ranks_binned_scan(cuda_device, name, D, N, T, shard):
     _run_virtual_ranks(name, D, N, T, shard, 2)
 
 
+@pytest.mark.parametrize("shard", [0, 1])
+@pytest.mark.parametrize("name,D,N,T", [("C3", 2, 3_000_000, 2), ("C4", 8, 4_000_000, 2)])
+def test_virtual_ranks_packet_owned_scan(cuda_device, name, D, N, T, shard):
+    """The same with every rank's scan forced onto k_scan_own (the default scan at C3-C5;
+    its write-back lands in the rank's peer-visible touch bitmap)."""
+    _run_virtual_ranks(name, D, N, T, shard, 3)
+
+
 def _run_virtual_ranks(name, D, N, T, shard, variant):
     p = dict(PRESETS[name])
     ranks = [asse.Asse(**dict(p, world=D, rank=d, frame_shard=shard)) for d in range(D)]
