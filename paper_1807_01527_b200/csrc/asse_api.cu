@@ -373,9 +373,9 @@ static cudaError_t coop_launch_own(Ctx* c, const uint2* pk, uint64_t n, const Ow
 
 static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const ScanParams& sp, cudaStream_t st) {
   const uint32_t G = c->bin_G, O = c->own_O;
-  const size_t sync_words = (2 * kOwnNB + (size_t)kOwnNB * O * kBinQG) * kBinPad;
+  const size_t sync_words = (2 * kOwnNB + (size_t)kOwnNB * O * kOwnQG) * kBinPad;
   if (!c->own_queue) {
-    CK(cudaMalloc(&c->own_queue, (size_t)kOwnNB * O * kBinQG * kOwnQCap * sizeof(uint2)));
+    CK(cudaMalloc(&c->own_queue, (size_t)kOwnNB * O * kOwnQG * kOwnQCap * sizeof(uint2)));
     CK(cudaMalloc(&c->own_sync, sync_words * 4));
   }
   const int dev = c->device & 63;
@@ -696,7 +696,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
         c->own_smem = own_smem_bytes(c->own_O, (uint32_t)std::min<uint64_t>(slice_words, 1u << 30), c->own_tile);
         c->own_ok = coop && p.r == 4 && (1u << lg_wpa) == c->wpa && c->own_O <= (uint32_t)c->sms && c->own_lg_wg <= p.u &&
                     c->own_O <= kOwnMaxOwners && c->own_O >= 2 &&
-                    (uint64_t)((c->sms + kBinQG - 1) / kBinQG) * kOwnCap <= kOwnQCap &&
+                    (uint64_t)((c->sms + kOwnQG - 1) / kOwnQG) * kOwnCap <= kOwnQCap &&
                     slice_words <= (1u << 20) && c->own_smem + 2048 <= (size_t)optin &&
                     !getenv("ASSE_SCAN_NO_OWN");
         if (c->own_ok) {

@@ -61,7 +61,14 @@ constexpr uint32_t kOwnNB = ASSE_OWN_NB;                   // queue buffers (rou
                                                            // 6 0.942, 8 0.927; tools/gpu_own_sweep4.sh)
 constexpr uint32_t kOwnNGR = ASSE_OWN_NGR;                 // drain groups (round t -> group t mod NGR)
 static_assert(kOwnNB % kOwnNGR == 0 && kOwnConsWarps % kOwnNGR == 0, "drain groups");
-constexpr uint32_t kOwnQCap = 2048;                        // ring entries per (buffer, owner, group) >= the
+#ifndef ASSE_OWN_QG
+#define ASSE_OWN_QG 4
+#endif
+constexpr uint32_t kOwnQG = ASSE_OWN_QG;                   // producer groups (CTA index mod QG), one ring each
+#ifndef ASSE_OWN_QCAP
+#define ASSE_OWN_QCAP 2048
+#endif
+constexpr uint32_t kOwnQCap = ASSE_OWN_QCAP;                        // ring entries per (buffer, owner, group) >= the
                                                            // producer group's bins (host-checked)
 constexpr uint32_t kOwnMaxOwners = 128;                   // F * NGRP: a power of two <= the SMs
 constexpr uint32_t kOwnMinTilesPerCta = 8;                 // below: k_scan is used
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   constexpr int kSig = 2 * kOwnNB;
   static_assert(kSig > kOwnNB + 1, "signal barrier ring");
   __shared__ __align__(8) uint64_t full[kOwnRing], empty[kOwnRing], sigbar[kSig];
-  __shared__ uint32_t slast[kOwnNB][kBinQG];     // drain: end of the last drained round per buffer/ring
+  __shared__ uint32_t slast[kOwnNB][kOwnQG];     // drain: end of the last drained round per buffer/ring
   const uint32_t G = gridDim.x, me = blockIdx.x, O = op.O;
   const uint32_t Op = (O + 3u) & ~3u;
   const bool owner = me < O;
@@ -271,7 +278,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         const uint32_t c = min(scount[sf * Op + my_o], cap);
         cnt = (c + 1u) & ~1u;
         if (c & 1u) stg[((size_t)sf * O + my_o) * cap + c] = make_uint2(0u, 0u);   // mask 0: no entry
-        if (cnt) off = atomicAdd(op.qcnt + (((size_t)bf * O + my_o) * kBinQG + (me % kBinQG)) * kBinPad, cnt);
+        if (cnt) off = atomicAdd(op.qcnt + (((size_t)bf * O + my_o) * kOwnQG + (me % kOwnQG)) * kBinPad, cnt);
       }
       c1 = clock64(); pc[1] += c1 - c0; c0 = c1;
       uint32_t seen = 0;
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       c1 = clock64(); pc[0] += c1 - c0; c0 = c1;
       if (t >= 1) {
         const uint2* stg_f = stg + (size_t)sf * O * cap;
-        uint2* qb = op.queue + ((size_t)bf * O * kBinQG + (me % kBinQG)) * kOwnQCap;
+        uint2* qb = op.queue + ((size_t)bf * O * kOwnQG + (me % kOwnQG)) * kOwnQCap;
         // two owners per step (one per half-warp), 16 B (two entries) per lane (measured
         // faster than the same copy with 32-bit offsets from per-round bases: 0.799 vs 0.812 ms)
         const uint32_t hl = lane & 15u, hw = lane >> 4;
@@ -335,7 +342,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         for (int k = 0; k < NS; ++k) {
           const uint32_t ow = warp + kOwnBinWarps * (2 * k + hw);
           if (2 * hl < c2[k]) {
-            uint4* dst = reinterpret_cast<uint4*>(qb + (size_t)ow * kBinQG * kOwnQCap);
+            uint4* dst = reinterpret_cast<uint4*>(qb + (size_t)ow * kOwnQG * kOwnQCap);
             dst[((of[k] >> 1) + hl) & (kOwnQCap / 2 - 1)] = v[k];
           }
         }
@@ -364,20 +371,20 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       c1 = clock64(); cwait += c1 - c0; c0 = c1;
       // the round's entries: QG ranges [start, end) of the owner's rings of buffer b; start =
       // end of the previous round in this buffer (slast, written by this group only)
-      uint32_t st[kBinQG], len[kBinQG], en[kBinQG], mx = 0;
+      uint32_t st[kOwnQG], len[kOwnQG], en[kOwnQG], mx = 0;
 #pragma unroll
-      for (int g = 0; g < (int)kBinQG; ++g) {
-        en[g] = ld_cg_u32(op.qcnt + (((size_t)b * O + me) * kBinQG + g) * kBinPad);
+      for (int g = 0; g < (int)kOwnQG; ++g) {
+        en[g] = ld_cg_u32(op.qcnt + (((size_t)b * O + me) * kOwnQG + g) * kBinPad);
         st[g] = t >= kOwnNB ? slast[b][g] : 0u;
         len[g] = en[g] - st[g];                  // entries (even)
         mx = max(mx, len[g]);
       }
-      const uint4* qb4 = reinterpret_cast<const uint4*>(op.queue + ((size_t)b * O + me) * kBinQG * kOwnQCap);
+      const uint4* qb4 = reinterpret_cast<const uint4*>(op.queue + ((size_t)b * O + me) * kOwnQG * kOwnQCap);
       constexpr int U = ASSE_OWN_U;              // 16-B groups in flight per thread per ring
       for (uint32_t e0 = gtid; 2 * e0 < mx; e0 += U * GT) {
-        uint4 v[kBinQG][U];
+        uint4 v[kOwnQG][U];
 #pragma unroll
-        for (int g = 0; g < (int)kBinQG; ++g)
+        for (int g = 0; g < (int)kOwnQG; ++g)
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint32_t e = e0 + u * GT;      // 16-B group index within the round's range
@@ -389,7 +396,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
             }
           }
 #pragma unroll
-        for (int g = 0; g < (int)kBinQG; ++g)
+        for (int g = 0; g < (int)kOwnQG; ++g)
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint4 x = v[g][u];
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       if (gtid == 0) {
         atomicAdd(cons_done + b * kBinPad, 1u);  // entries consumed before
 #pragma unroll
-        for (int g = 0; g < (int)kBinQG; ++g) slast[b][g] = en[g];
+        for (int g = 0; g < (int)kOwnQG; ++g) slast[b][g] = en[g];
       }
       c1 = clock64(); cwork += c1 - c0; c0 = c1;
     }
