@@ -108,11 +108,14 @@ const char* asse_last_error(const void* ctx);
 /* Enable/disable per-kernel CUDA-event timing (asse_stats.*_ms). Default off. */
 asse_status asse_set_timing(void* ctx, int enable);
 
-/* Scan kernel selection: 0 = automatic (default: the binned scan k_scan_bin when its
- * part of the touch bitmap fits the SMs' shared memory, r = 4, and a call brings at least
- * 8 rounds of packets per SM, else k_scan), 1 = always k_scan (one RED.OR per SetAT into
- * the L2-resident bitmap), 2 = always k_scan_bin (ASSE_E_PARAM if unavailable). Both
- * produce the identical touch bitmap (SetAT is idempotent). */
+/* Scan kernel selection: 0 = automatic (default: the packet-owned scan k_scan_own when the
+ * geometry admits it — r = 4, g/32 a power of two, an owner slice of r x 2^c ATVs x g/32/NGRP
+ * words fits one SM's shared memory — and a call brings at least 8 rounds of packets per SM;
+ * else the binned scan k_scan_bin under the same size rule when its part of the touch bitmap
+ * fits the SMs' shared memory; else k_scan), 1 = always k_scan (one RED.OR per SetAT into the
+ * L2-resident bitmap), 2 = always k_scan_bin, 3 = always k_scan_own (ASSE_E_PARAM if the
+ * chosen kernel is unavailable). All produce the identical touch bitmap (SetAT is
+ * idempotent), so pools and reports do not depend on the choice. */
 asse_status asse_set_scan_variant(void* ctx, int variant);
 
 /* Alg. 3 "Scan IP pair" for n_pairs packets of the current slice.

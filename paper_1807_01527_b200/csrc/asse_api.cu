@@ -1055,7 +1055,6 @@ static unsigned fold_blocks(const Ctx* c) {
 // eagerly (world > 1 with a device barrier) or captured once into a CUDA graph per
 // (timing, mode) and replayed every slice; the per-slice ACT base comes from d_clock.
 static asse_status enqueue_end_slice(Ctx* c, uint32_t mode, bool timing, bool capturing) {
-  const asse_config& p = c->cfg;
   cudaStream_t s = c->stream;
   // events recorded inside a captured graph must be external event-record nodes
   auto rec = [&](int i) {
