@@ -165,7 +165,8 @@ class Asse:
         self._check(self._L.asse_set_timing(self._h, 1 if on else 0))
 
     def set_scan_variant(self, variant):
-        """0 = automatic, 1 = k_scan (direct RED.OR), 2 = k_scan_bin (shared-memory bins)."""
+        """0 = automatic, 1 = k_scan (direct RED.OR), 2 = k_scan_bin (shared-memory bins),
+        3 = k_scan_own (packet-owned shared-memory slices; the automatic choice at C3-C5)."""
         self._check(self._L.asse_set_scan_variant(self._h, int(variant)))
 
     def scan_slice(self, pairs, n=None, stream=None):
