@@ -23,6 +23,19 @@
 #pragma once
 #include "asse_scan_bin.cuh"
 
+// ASSE_OWN_DEBUG_BOUNDS=1: device asserts on every index the kernel derives (owner, slot,
+// slice word, ring ranges, write-back word) — the bounds check used on the GPU pool, where
+// compute-sanitizer is unavailable (tools/gpu_own_bounds.sh runs the parity tests with it)
+#ifndef ASSE_OWN_DEBUG_BOUNDS
+#define ASSE_OWN_DEBUG_BOUNDS 0
+#endif
+#if ASSE_OWN_DEBUG_BOUNDS
+#include <cassert>
+#define OWN_ASSERT(x) assert(x)
+#else
+#define OWN_ASSERT(x) ((void)0)
+#endif
+
 namespace asse {
 
 #ifndef ASSE_OWN_BIN_WARPS
@@ -151,6 +164,7 @@ __device__ __forceinline__ void own_apply(const OwnScanParams& op, uint32_t* sbm
   for (int y = 0; y < 4; ++y) {
     const uint32_t x = (uint32_t)(D >> Geo::shift(op, y)) & Geo::cmask(op);
     const uint32_t w = (((((uint32_t)y << Geo::c(op)) | x) << Geo::lg_wg(op)) | sub);
+    OWN_ASSERT(w < ((uint32_t)op.sp.r << (op.sp.c + op.lg_wg)) && m != 0u);
     atomicOr(sbm + w, m);
   }
 }
@@ -173,6 +187,7 @@ __device__ __forceinline__ void own_bin_two(const OwnScanParams& op, const uint4
   const uint32_t fm = Geo::fmask(op);
   const uint32_t o0 = ((h0 & fm) << Geo::lg_ngrp(op)) | (i0 >> gs);
   const uint32_t o1 = ((h1 & fm) << Geo::lg_ngrp(op)) | (i1 >> gs);
+  OWN_ASSERT(!valid || (o0 < op.O && o1 < op.O));
   const uint32_t pos0 = atoms_inc(valid ? scount_s + 4u * o0 : scount_dummy);
   const uint32_t pos1 = atoms_inc(valid ? scount_s + 4u * o1 : scount_dummy);
   const bool ok0 = pos0 < cap, ok1 = pos1 < cap;
@@ -279,6 +294,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         cnt = (c + 1u) & ~1u;
         if (c & 1u) stg[((size_t)sf * O + my_o) * cap + c] = make_uint2(0u, 0u);   // mask 0: no entry
         if (cnt) off = atomicAdd(op.qcnt + (((size_t)bf * O + my_o) * kOwnQG + (me % kOwnQG)) * kBinPad, cnt);
+        OWN_ASSERT(cnt <= cap + 1u && (cnt & 1u) == 0u && (off & 1u) == 0u);
       }
       c1 = clock64(); pc[1] += c1 - c0; c0 = c1;
       uint32_t seen = 0;
@@ -377,6 +393,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         en[g] = ld_cg_u32(op.qcnt + (((size_t)b * O + me) * kOwnQG + g) * kBinPad);
         st[g] = t >= kOwnNB ? slast[b][g] : 0u;
         len[g] = en[g] - st[g];                  // entries (even)
+        OWN_ASSERT(len[g] <= kOwnQCap && (len[g] & 1u) == 0u);
         mx = max(mx, len[g]);
       }
       const uint4* qb4 = reinterpret_cast<const uint4*>(op.queue + ((size_t)b * O + me) * kOwnQG * kOwnQCap);
@@ -434,6 +451,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         const uint32_t w = q << 1;
         const uint32_t yx = w >> op.lg_wg, sub = w & (wg - 1u);
         const uint32_t y = yx >> p.c, x = yx & p.cmask;
+        OWN_ASSERT((size_t)(y * row_words + x) * p.wpa + gbase + sub + 1 < (size_t)p.r * row_words * p.wpa);
         uint2* gd = reinterpret_cast<uint2*>(p.touch + (size_t)(y * row_words + x) * p.wpa + gbase + sub);
         uint2 gv;
         asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(gv.x), "=r"(gv.y) : "l"(gd));

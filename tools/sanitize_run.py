@@ -71,3 +71,24 @@ for t in range(3):
     b.end_slice_async(1)
     torch.cuda.synchronize()
 print("C3 bin last", len(b.end_slice_wait()), flush=True)
+
+# packet-owned scan (k_scan_own) on the C3 geometry (constant-folded instantiation) and on
+# C2 (runtime geometry): ragged + misaligned calls, a hot-spot overflow slice
+for name in ("C3", "C2"):
+    po = dict(PRESETS[name])
+    o = asse.Asse(**po)
+    o.set_scan_variant(3)
+    go = Generator(name, N=400_001)
+    for t in range(2):
+        pk = go.slice(t)
+        d = dev(pk)
+        o.scan_slice(d.data_ptr() + 8, len(pk) - 1)
+        o.scan_slice(d.data_ptr(), 3)
+        print(name, "own", t, len(o.end_slice(1)), flush=True)
+    hot = np.stack([np.full(300_000, 0x0A000001, np.uint32),
+                    np.random.default_rng(1).integers(0, 2 ** 32, 300_000, dtype=np.uint32)], 1)
+    d = dev(hot)
+    o.scan_slice(d)
+    print(name, "own hot", len(o.end_slice(1)), flush=True)
+torch.cuda.synchronize()
+print("sanitize run (k_scan_own) ok", flush=True)
