@@ -1,0 +1,15 @@
+mkdir -p gpurun_out
+L=paper_1807_01527_b200/libasse.so
+cp $L /tmp/libasse_orig.so
+cp tools/variants/libasse_qg6u2.so $L
+timeout 900 python -m pytest tests/test_gpu_scan_own.py tests/test_gpu_multi.py -x -q --timeout=300 -k "owned or packet_owned" > gpurun_out/own23_pytest.log 2>&1; echo "pytest(qg6u2) rc=$?"; tail -2 gpurun_out/own23_pytest.log
+one() {
+  cp tools/variants/libasse_$1.so $L
+  timeout 300 python bench.py --workload $2 --steps 20 --warmup 3 --no-e2e --no-cpu --scan-variant 3 > gpurun_out/sw_$1_$2.log 2>&1
+  python -c "import json,sys; d=json.loads(open('gpurun_out/sw_$1_$2.log').read().strip().splitlines()[-1]); print('$1 $2', round(d['value'],2), 'Gpps scan_ms', round(d['roofline']['avg_launch_ms'],4))" 2>&1 | tail -1
+}
+for r in 1 2; do for v in def qg8u1 qg6u1 qg6u2 qg5u2; do one $v C5; done; done
+
+cp tools/variants/libasse_def.so $L
+ASSE_SCAN_PROF=1 timeout 300 python bench.py --workload C5 --steps 3 --warmup 3 --no-e2e --no-cpu 2>&1 | grep "^k_scan_own" | tail -1
+cp /tmp/libasse_orig.so $L
