@@ -107,3 +107,23 @@ def test_owned_on_caller_stream_and_host_ingest(cuda_device):
     assert (rd["ip"] == ro["ip"]).all() and (rd["nat"] == ro["nat"]).all()
     assert (dev.pool() == ora.pool()).all()
     assert dev.stats()["scan_own_launches"] >= 3
+
+
+def test_owned_equals_direct_over_many_slices(cuda_device):
+    """Soak: 12 consecutive C3 slices (20M packets each, ~66 rounds per launch) through the
+    packet-owned and the direct kernel; pools and reports identical after every slice, so
+    no round-synchronisation race shows up over ~800 rounds."""
+    import torch
+    p = dict(PRESETS["C3"])
+    own, direct = asse.Asse(**p), asse.Asse(**p)
+    own.set_scan_variant(3)
+    direct.set_scan_variant(1)
+    g = Generator("C3")
+    for t in range(12):
+        d = torch.from_numpy(g.slice(t, threads=16).view(np.int32).reshape(-1)).cuda()
+        own.scan_slice(d)
+        direct.scan_slice(d)
+        ro, rd = own.end_slice(1), direct.end_slice(1)
+        assert len(ro) == len(rd) and (ro["ip"] == rd["ip"]).all() and (ro["nat"] == rd["nat"]).all(), t
+        assert (own.pool() == direct.pool()).all(), t
+    assert own.stats()["scan_own_launches"] == 12 and direct.stats()["scan_own_launches"] == 0
