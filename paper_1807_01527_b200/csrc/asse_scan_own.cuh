@@ -54,7 +54,7 @@ namespace asse {
 #define ASSE_OWN_X2 1
 #endif
 #ifndef ASSE_OWN_U
-#define ASSE_OWN_U 2
+#define ASSE_OWN_U 1
 #endif
 // warps (measured at C5 on B200, tools/gpu_own_sweep2.sh, gpu_own13.sh): with runtime geometry
 // 16 binning + 8 / 10 / 12 / 14 draining warps 0.98 / 1.07 / 0.94 / 0.95 ms; with the C3
@@ -75,13 +75,16 @@ constexpr uint32_t kOwnNB = ASSE_OWN_NB;                   // queue buffers (rou
 constexpr uint32_t kOwnNGR = ASSE_OWN_NGR;                 // drain groups (round t -> group t mod NGR)
 static_assert(kOwnNB % kOwnNGR == 0 && kOwnConsWarps % kOwnNGR == 0, "drain groups");
 #ifndef ASSE_OWN_QG
-#define ASSE_OWN_QG 4
+#define ASSE_OWN_QG 6
 #endif
 constexpr uint32_t kOwnQG = ASSE_OWN_QG;                   // producer groups (CTA index mod QG), one ring each
+                                                           // per (buffer, owner): C5 2 / 4 / 6 / 8 groups
+                                                           // 0.807 / 0.795 / 0.791 / 1.22 ms
 #ifndef ASSE_OWN_QCAP
-#define ASSE_OWN_QCAP 2048
+#define ASSE_OWN_QCAP 1024
 #endif
-constexpr uint32_t kOwnQCap = ASSE_OWN_QCAP;                        // ring entries per (buffer, owner, group) >= the
+constexpr uint32_t kOwnQCap = ASSE_OWN_QCAP;
+static_assert((kOwnQCap & (kOwnQCap - 1)) == 0, "ring index is masked");                        // ring entries per (buffer, owner, group) >= the
                                                            // producer group's bins (host-checked)
 constexpr uint32_t kOwnMaxOwners = 128;                   // F * NGRP: a power of two <= the SMs
 constexpr uint32_t kOwnMinTilesPerCta = 8;                 // below: k_scan is used

@@ -8,7 +8,7 @@ import pytest
 
 from gen import PRESETS
 
-KOWN_CAP, KBIN_QG, KOWN_QCAP, KOWN_MAX_OWNERS, KOWN_RING = 30, 4, 2048, 128, 2   # asse_scan_own.cuh
+KOWN_CAP, KBIN_QG, KOWN_QCAP, KOWN_MAX_OWNERS, KOWN_RING = 30, 6, 1024, 128, 2   # asse_scan_own.cuh
 OPTIN = 232448                                                                     # B200 opt-in smem / block
 
 
