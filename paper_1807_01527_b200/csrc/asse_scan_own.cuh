@@ -39,7 +39,7 @@
 namespace asse {
 
 #ifndef ASSE_OWN_BIN_WARPS
-#define ASSE_OWN_BIN_WARPS 16
+#define ASSE_OWN_BIN_WARPS 8
 #endif
 #ifndef ASSE_OWN_CONS_WARPS
 #define ASSE_OWN_CONS_WARPS 8
@@ -51,7 +51,7 @@ namespace asse {
 #define ASSE_OWN_NGR 2
 #endif
 #ifndef ASSE_OWN_X2
-#define ASSE_OWN_X2 1
+#define ASSE_OWN_X2 0
 #endif
 #ifndef ASSE_OWN_U
 #define ASSE_OWN_U 1
@@ -59,7 +59,11 @@ namespace asse {
 // warps (measured at C5 on B200, tools/gpu_own_sweep2.sh, gpu_own13.sh): with runtime geometry
 // 16 binning + 8 / 10 / 12 / 14 draining warps 0.98 / 1.07 / 0.94 / 0.95 ms; with the C3
 // geometry folded (cheaper drain) 6 / 8 / 10 / 12 warps 0.95 / 0.82 / 0.86 / 0.84 ms, 8 warps
-// with two 16-B groups in flight per ring 0.81 ms
+// with two 16-B groups in flight per ring 0.81 ms. Binning warps (8 draining, 6 rings, one 16-B
+// group in flight, tools/gpu_own28-30.sh): 16 / 14 / 12 / 10 / 8 / 6 / 4 warps 0.79 / 0.79 /
+// 0.77 / 0.82 / 0.74 / 0.89 / 1.32 ms — fewer warps leave each thread more registers (96 at
+// 8 warps: no address rematerialisation in the binning loop); 8 warps with 6 or 12 draining
+// warps 0.86 / 1.16 ms
 constexpr int kOwnBinWarps = ASSE_OWN_BIN_WARPS;           // binning + shipping warps
 constexpr int kOwnConsWarps = ASSE_OWN_CONS_WARPS;         // queue-draining warps, two groups (round parity)
 constexpr int kOwnConsWarp0 = kOwnBinWarps;
