@@ -285,7 +285,12 @@ template <int CB, bool WEIGH = false> constexpr size_t fold_smem() {
 // its per-lane constants stay fixed; the ATV weight is summed across the 2^QL warps
 // with one packed shared-memory atomic (weight << 8 | arrival count).
 template <int CB, int LPAL, bool WEIGH = false, int QL = 0>
-__global__ void __launch_bounds__(fold_threads<CB, WEIGH>(), CB == 1 ? 3 : 2) k_fold(FoldParams p) {
+// u8 fold: 2 CTAs per SM (84 registers) beat 3 (64 registers, operands rematerialised):
+// C3 fold 63.2 -> 60.3 us (tools/gpu_fold1.sh)
+#ifndef ASSE_FOLD_MINB1
+#define ASSE_FOLD_MINB1 2
+#endif
+__global__ void __launch_bounds__(fold_threads<CB, WEIGH>(), CB == 1 ? ASSE_FOLD_MINB1 : 2) k_fold(FoldParams p) {
   using S = Swar<CB>;
   constexpr int NW = S::NW, EPW = S::EPW, EB = S::EB;
   constexpr uint32_t G = S::G;
