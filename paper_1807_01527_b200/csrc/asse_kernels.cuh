@@ -290,7 +290,10 @@ template <int CB, int LPAL, bool WEIGH = false, int QL = 0>
 #ifndef ASSE_FOLD_MINB1
 #define ASSE_FOLD_MINB1 2
 #endif
-__global__ void __launch_bounds__(fold_threads<CB, WEIGH>(), CB == 1 ? ASSE_FOLD_MINB1 : 2) k_fold(FoldParams p) {
+#ifndef ASSE_FOLD_MINB2
+#define ASSE_FOLD_MINB2 2   // u16: 1 CTA per SM (133 registers) measured slower: C4 fold 117 vs 106 us
+#endif
+__global__ void __launch_bounds__(fold_threads<CB, WEIGH>(), CB == 1 ? ASSE_FOLD_MINB1 : ASSE_FOLD_MINB2) k_fold(FoldParams p) {
   using S = Swar<CB>;
   constexpr int NW = S::NW, EPW = S::EPW, EB = S::EB;
   constexpr uint32_t G = S::G;
