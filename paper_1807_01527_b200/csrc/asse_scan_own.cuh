@@ -48,7 +48,7 @@ namespace asse {
 #define ASSE_OWN_NB 8
 #endif
 #ifndef ASSE_OWN_NGR
-#define ASSE_OWN_NGR 2
+#define ASSE_OWN_NGR 4
 #endif
 #ifndef ASSE_OWN_X2
 #define ASSE_OWN_X2 0
@@ -78,6 +78,9 @@ constexpr uint32_t kOwnNB = ASSE_OWN_NB;                   // queue buffers (rou
                                                            // 6 0.942, 8 0.927; tools/gpu_own_sweep4.sh)
 constexpr uint32_t kOwnNGR = ASSE_OWN_NGR;                 // drain groups (round t -> group t mod NGR)
 static_assert(kOwnNB % kOwnNGR == 0 && kOwnConsWarps % kOwnNGR == 0, "drain groups");
+static_assert(2 + kOwnNGR <= 8, "named barriers 2 .. 1 + NGR must stay below the compute barrier 8");
+// drain groups (8 binning / 8 draining warps, tools/gpu_own32-33.sh): 1 / 2 / 4 groups
+// 0.966 / 0.739 / 0.716 ms at C5
 #ifndef ASSE_OWN_QG
 #define ASSE_OWN_QG 6
 #endif
