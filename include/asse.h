@@ -88,10 +88,13 @@ typedef struct {
   uint32_t scan_bin_ok;          /* 1 if k_scan_bin is available for this geometry/device */
   uint32_t scan_own_launches;    /* cumulative launches of the packet-owned scan (k_scan_own) */
   uint32_t scan_own_ok;          /* 1 if k_scan_own is available for this geometry/device */
+  uint32_t host_barriers;        /* cumulative host barriers (sync_mode 2) */
+  uint32_t pad0;
 } asse_stats;
 
-/* Validate a configuration (completeness/redundancy P:315-324, A10; the device
- * path additionally needs g % 128 == 0 and g <= 512 in this version).
+/* Validate a configuration (completeness/redundancy P:315-324, A10). The device path
+ * additionally needs g a power of two in [128, 4096], c + u <= 24, 2 <= r <= 8,
+ * k <= 16383 and world <= 16 (frame_shard: world divides 2^u).
  * why: caller-owned buffer of n bytes for a message (may be NULL). */
 asse_status asse_validate(const asse_config* cfg, char* why, size_t n);
 
@@ -122,8 +125,11 @@ asse_status asse_set_scan_variant(void* ctx, int variant);
  * d_pairs: caller-owned DEVICE buffer of 2*n_pairs uint32 [aip0,bip0,aip1,...]
  *          (A33), 8-byte aligned; it must stay valid until the scan has run
  *          (stream-ordered on `stream`; asse_end_slice synchronizes).
- * stream:  cudaStream_t to launch on (NULL = the context's stream). The context's
- *          stream is made to wait on it, so end_slice sees every scan (A34).
+ * stream:  cudaStream_t to launch on (NULL = the context's stream). A caller stream is
+ *          first made to wait for the context's stream (a pending asse_end_slice_async
+ *          still folds and clears the touch bitmap), then the context's stream is made
+ *          to wait on it, so end_slice sees every scan (A34). Scans of one context are
+ *          serialised whatever streams they are issued on.
  * Asynchronous; may be called any number of times per slice; n_pairs = 0 is legal. */
 asse_status asse_scan_slice(void* ctx, const uint32_t* d_pairs, uint64_t n_pairs, void* stream);
 
@@ -185,13 +191,14 @@ asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint
 asse_status asse_export_pool(void* ctx, uint16_t* h_out, uint64_t n);
 
 /* Checkpoint: write the pool codes, slice index t and ACT
- * base C0 with the parameters (k, k', r, c, u, s, g, theta, seed) and a magic/version
- * header to `path`. Take it after asse_end_slice (touches of a slice still being
+ * base C0 with the parameters (k, k', r, c, u, s, g, theta, seed, mangle, frame sharding)
+ * and a magic/version (3) header to `path`. Take it after asse_end_slice (touches of a slice still being
  * scanned are not saved). ASSE_E_PARAM on I/O errors. */
 asse_status asse_save_state(void* ctx, const char* path);
 
 /* Restore a checkpoint into a context created with the same parameters (rejects any
- * mismatch with ASSE_E_PARAM); pending touches of the context are discarded. */
+ * parameter mismatch, another version, or a clock with C0 != t mod 2k, with ASSE_E_PARAM);
+ * pending touches of the context are discarded. */
 asse_status asse_load_state(void* ctx, const char* path);
 
 /* Number of ATs in this context's pool (r * 2^u * 2^c * g, or its frames' share in option S). */
@@ -222,10 +229,37 @@ void* asse_get_stream(const void* ctx);
  *            stream-ordered cross-GPU barrier when sync_mode == 0.
  * sync_mode: 0 = device barrier over the signal pads (one process per GPU);
  *            1 = caller-ordered (all ranks' scans complete before any merge, all
- *                merges complete before any end_slice; used by single-GPU tests).
+ *                merges complete before any end_slice; used by single-GPU tests);
+ *            2 = host barrier: at each cross-rank point end_slice synchronises the
+ *                context's stream and calls the callback set by asse_set_host_barrier
+ *                (e.g. a torch.distributed barrier); no kernel waits on another rank's
+ *                kernel, so ranks may share a GPU. signal may be NULL.
  * Buffers are caller-owned and must outlive the context. */
 asse_status asse_attach_peers(void* ctx, void* const* touch, void* const* merged,
                               void* const* signal, void* const* exchange, uint32_t sync_mode);
+
+/* sync_mode 2: the host barrier across all ranks. fn(arg) must return 0 after every rank
+ * has called it for the same barrier instance (nonzero: end_slice fails with ASSE_E_PEER).
+ * end_slice calls it 2 times per slice (option R: before the merge, after the merge;
+ * option S: before the merge, before the report gather). */
+typedef int (*asse_host_barrier_fn)(void* arg);
+asse_status asse_set_host_barrier(void* ctx, asse_host_barrier_fn fn, void* arg);
+
+/* CUDA IPC peer buffers (one process per rank on one node; NVLink peer access is enabled
+ * lazily on open). asse_ipc_alloc: zeroed device buffer of `bytes` on `device` (library-
+ * owned until asse_ipc_free(ptr, 0)) and its 64-byte handle (caller-owned `handle`);
+ * asse_ipc_open: map another process's buffer, released with asse_ipc_free(ptr, 1).
+ * A process cannot open its own handle (ASSE_E_PEER). */
+#define ASSE_IPC_HANDLE_BYTES 64
+asse_status asse_ipc_alloc(int32_t device, uint64_t bytes, void** d_ptr, uint8_t* handle);
+asse_status asse_ipc_open(const uint8_t* handle, int32_t device, void** d_ptr);
+asse_status asse_ipc_free(void* d_ptr, int32_t opened);
+
+/* Self-test of the cross-rank device barrier used by sync_mode 0 (k_barrier): `world`
+ * ranks are played by the blocks of ONE cooperative kernel on `device` (co-resident by
+ * construction), each crossing 2 * epochs barriers and checking after each that it sees
+ * every rank's data of that epoch. *errors = number of stale reads (0 = pass). */
+asse_status asse_selftest_barrier(int32_t device, uint32_t world, uint32_t epochs, uint64_t* errors);
 
 /* Bytes of one touch bitmap (whole geometry): r * 2^u * 2^c * g / 8. */
 uint64_t asse_bitmap_bytes(const void* ctx);

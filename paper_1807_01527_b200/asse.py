@@ -27,7 +27,8 @@ SYMBOLS = ["asse_validate", "asse_init", "asse_destroy", "asse_last_error", "ass
            "asse_get_stats", "asse_get_stream", "asse_attach_peers", "asse_bitmap_bytes",
            "asse_merge", "asse_query_window", "asse_save_state", "asse_load_state",
            "asse_merged_bytes", "asse_exchange_bytes", "asse_end_slice_begin", "asse_end_slice_async",
-           "asse_end_slice_wait"]
+           "asse_end_slice_wait", "asse_set_host_barrier", "asse_ipc_alloc", "asse_ipc_open",
+           "asse_ipc_free", "asse_selftest_barrier"]
 
 
 class AsseError(RuntimeError):
@@ -58,13 +59,16 @@ class Stats(ctypes.Structure):
                 ("last_n_above", ctypes.c_uint32), ("w_theta", ctypes.c_uint32),
                 ("code_bytes", ctypes.c_uint32), ("scan_bin_launches", ctypes.c_uint32),
                 ("scan_rows_red", ctypes.c_uint32), ("scan_bin_ok", ctypes.c_uint32),
-                ("scan_own_launches", ctypes.c_uint32), ("scan_own_ok", ctypes.c_uint32)]
+                ("scan_own_launches", ctypes.c_uint32), ("scan_own_ok", ctypes.c_uint32),
+                ("host_barriers", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
 
 
 _lib = None
+HOST_BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+IPC_HANDLE_BYTES = 64
 
 
 def load_library(path=LIB_PATH):
@@ -106,6 +110,11 @@ def load_library(path=LIB_PATH):
         "asse_query_window": (i32, [vp, u32, vp, u32, ctypes.POINTER(u32), u32]),
         "asse_save_state": (i32, [vp, ctypes.c_char_p]),
         "asse_load_state": (i32, [vp, ctypes.c_char_p]),
+        "asse_set_host_barrier": (i32, [vp, HOST_BARRIER_FN, vp]),
+        "asse_ipc_alloc": (i32, [i32, u64, ctypes.POINTER(vp), ctypes.c_char_p]),
+        "asse_ipc_open": (i32, [ctypes.c_char_p, i32, ctypes.POINTER(vp)]),
+        "asse_ipc_free": (i32, [vp, i32]),
+        "asse_selftest_barrier": (i32, [i32, u32, u32, ctypes.POINTER(u64)]),
     }
     for name, (rt, at) in sigs.items():
         f = getattr(L, name)
@@ -282,8 +291,53 @@ class Asse:
         self._check(self._L.asse_attach_peers(self._h, arr(touch), arr(merged), arr(signal),
                                               arr(exchange), sync_mode))
 
+    def set_host_barrier(self, fn):
+        """sync_mode 2: fn() is called by end_slice at each cross-rank point (after this
+        rank's queued work completed) and must return once every rank has called it."""
+        def _cb(_arg):
+            try:
+                fn()
+                return 0
+            except Exception:
+                return 1
+        self._barrier_cb = HOST_BARRIER_FN(_cb)      # kept alive with the context
+        self._check(self._L.asse_set_host_barrier(self._h, self._barrier_cb, None))
+
     def end_slice_begin(self):
         self._check(self._L.asse_end_slice_begin(self._h))
 
     def merge(self):
         self._check(self._L.asse_merge(self._h))
+
+
+def ipc_alloc(nbytes, device=0):
+    """Zeroed device buffer for CUDA IPC sharing: returns (ptr, 64-byte handle)."""
+    ptr, h = ctypes.c_void_p(), ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    st = load_library().asse_ipc_alloc(device, nbytes, ctypes.byref(ptr), h)
+    if st != OK:
+        raise AsseError(st, "asse_ipc_alloc")
+    return ptr.value, h.raw
+
+
+def ipc_open(handle, device=0):
+    """Map another process's asse_ipc_alloc buffer; returns the device pointer."""
+    ptr = ctypes.c_void_p()
+    st = load_library().asse_ipc_open(bytes(handle), device, ctypes.byref(ptr))
+    if st != OK:
+        raise AsseError(st, "asse_ipc_open")
+    return ptr.value
+
+
+def ipc_free(ptr, opened):
+    st = load_library().asse_ipc_free(ptr, 1 if opened else 0)
+    if st != OK:
+        raise AsseError(st, "asse_ipc_free")
+
+
+def selftest_barrier(world, epochs, device=0):
+    """Stale reads seen by the device barrier protocol run as one cooperative kernel."""
+    err = ctypes.c_uint64()
+    st = load_library().asse_selftest_barrier(device, world, epochs, ctypes.byref(err))
+    if st != OK:
+        raise AsseError(st, "asse_selftest_barrier")
+    return err.value

@@ -102,6 +102,8 @@ struct Ctx {
   uint64_t stage_pairs = 0;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_scanned[2] = {nullptr, nullptr};
   cudaEvent_t ev_join = nullptr;
+  cudaEvent_t ev_order = nullptr;     // context stream -> caller stream (asse_scan_slice)
+  cudaEvent_t ev_scan_last = nullptr; // last scan of this context: scans on any stream are serialised
   // timing
   bool timing = false;
   std::vector<cudaEvent_t> ev_free;
@@ -116,7 +118,9 @@ struct Ctx {
   cudaEvent_t ev_collect = nullptr;
   // peers
   bool peers = false;
-  uint32_t sync_mode = 0, epoch = 0;
+  uint32_t sync_mode = 0, epoch = 0;  // 0 device barrier, 1 caller-ordered, 2 host barrier
+  asse_host_barrier_fn host_barrier = nullptr;   // sync_mode 2
+  void* host_barrier_arg = nullptr;
   void* peer_touch[kMaxWorld] = {nullptr};
   void* peer_merged[kMaxWorld] = {nullptr};
   void* peer_xchg[kMaxWorld] = {nullptr};
@@ -210,6 +214,8 @@ static void free_all(Ctx* c) {
     if (c->ev_scanned[q]) cudaEventDestroy(c->ev_scanned[q]);
   }
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_order) cudaEventDestroy(c->ev_order);
+  if (c->ev_scan_last) cudaEventDestroy(c->ev_scan_last);
   for (auto& pr : c->scan_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto e : c->ev_free) cudaEventDestroy(e);
   for (auto e : c->ev) if (e) cudaEventDestroy(e);
@@ -459,6 +465,10 @@ static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cuda
     CK(cudaEventRecord(e0, st));
   }
   const uint2* pk = reinterpret_cast<const uint2*>(d_pairs);
+  // every scan of this context waits for the previous one, whatever stream either runs on:
+  // the owner write-backs of k_scan_bin / k_scan_own read-OR-write touch words, which a
+  // concurrent k_scan's REDs into the same bitmap could otherwise interleave with
+  CK(cudaStreamWaitEvent(st, c->ev_scan_last, 0));
   const bool use_own = c->own_ok && (c->scan_variant == 3 ||
                                      (c->scan_variant == 0 && tiles * kScanTileBytes >= (uint64_t)c->bin_G * kOwnMinTilesPerCta * c->own_tile));
   const bool use_bin = !use_own && c->bin_ok && (c->scan_variant == 2 ||
@@ -474,6 +484,7 @@ static asse_status launch_scan(Ctx* c, const uint32_t* d_pairs, uint64_t n, cuda
     else k_scan<2><<<(unsigned)blocks, kScanThreads, kScanSmem, st>>>(pk, n, p);
   }
   CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev_scan_last, st));
   LAUNCHED(c);
   c->stats.scan_launches++;
   c->stats.packets_scanned += n;
@@ -530,6 +541,19 @@ static asse_status do_merge(Ctx* c) {
   k_merge_or<<<(unsigned)blocks, 256, 0, c->stream>>>(mp);
   CK(cudaGetLastError());
   LAUNCHED(c);
+  return ASSE_OK;
+}
+
+// Cross-rank barrier of the eager end_slice (sync_mode 0: stream-ordered device barrier
+// over the peer signal pads; sync_mode 2: this rank's queued work completes, then the
+// caller's host barrier — no kernel ever waits for another rank's kernel).
+static asse_status device_barrier(Ctx* c);
+static asse_status rank_barrier(Ctx* c) {
+  if (c->sync_mode == 0) return device_barrier(c);
+  CK(cudaStreamSynchronize(c->stream));
+  if (!c->host_barrier) { c->err = "sync_mode 2 without asse_set_host_barrier"; return ASSE_E_PEER; }
+  if (c->host_barrier(c->host_barrier_arg) != 0) { c->err = "host barrier callback failed"; return ASSE_E_PEER; }
+  c->stats.host_barriers++;
   return ASSE_OK;
 }
 
@@ -791,6 +815,9 @@ asse_status asse_init(const asse_config* cfg, void** out) {
     CKI(cudaEventCreateWithFlags(&c->ev_scanned[q], cudaEventDisableTiming));
   }
   CKI(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  CKI(cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming));
+  CKI(cudaEventCreateWithFlags(&c->ev_scan_last, cudaEventDisableTiming));
+  CKI(cudaEventRecord(c->ev_scan_last, c->stream));
   // InitAT: every AT = 2k
   {
     uint64_t blocks = std::min<uint64_t>((c->n_at + 255) / 256, (uint64_t)c->sms * 16);
@@ -845,6 +872,12 @@ asse_status asse_scan_slice(void* ctx, const uint32_t* d_pairs, uint64_t n_pairs
   if (n_pairs && (!d_pairs || ((uintptr_t)d_pairs & 7))) { c->err = "d_pairs must be 8-byte aligned device memory"; return ASSE_E_PARAM; }
   CK(cudaSetDevice(c->device));
   cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  if (st != c->stream) {
+    // a caller stream first waits for everything queued on the context stream: an
+    // asse_end_slice_async's k_fold still reads and clears the touch bitmap this scan writes
+    CK(cudaEventRecord(c->ev_order, c->stream));
+    CK(cudaStreamWaitEvent(st, c->ev_order, 0));
+  }
   asse_status s = launch_scan(c, d_pairs, n_pairs, st);
   if (s != ASSE_OK) return s;
   if (st != c->stream) {
@@ -891,7 +924,7 @@ asse_status asse_attach_peers(void* ctx, void* const* touch, void* const* merged
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   if (c->cfg.world < 2) { c->err = "attach_peers needs world >= 2"; return ASSE_E_PEER; }
-  if (sync_mode > 1) { c->err = "sync_mode is 0 or 1"; return ASSE_E_PARAM; }
+  if (sync_mode > 2) { c->err = "sync_mode is 0, 1 or 2"; return ASSE_E_PARAM; }
   if (!touch || !merged || (sync_mode == 0 && !signal) || (c->shard && !exchange)) {
     c->err = "missing peer arrays"; return ASSE_E_PEER;
   }
@@ -1066,11 +1099,11 @@ static asse_status enqueue_end_slice(Ctx* c, uint32_t mode, bool timing, bool ca
   const uint32_t* src = c->touch;
   asse_status st;
   if (c->peers) {
-    if (c->sync_mode == 0) {
-      if ((st = device_barrier(c)) != ASSE_OK) return st;   // every rank's scans (and gathers) done
+    if (c->sync_mode != 1) {
+      if ((st = rank_barrier(c)) != ASSE_OK) return st;   // every rank's scans (and gathers) done
       if (c->shard) CK(cudaMemsetAsync(c->xchg, 0, 64, s));   // exchange count of this slice
       if ((st = do_merge(c)) != ASSE_OK) return st;
-      if (!c->shard && (st = device_barrier(c)) != ASSE_OK) return st;   // every shard merged
+      if (!c->shard && (st = rank_barrier(c)) != ASSE_OK) return st;   // every shard merged
     }
     src = c->merged;
   }
@@ -1090,7 +1123,7 @@ static asse_status enqueue_end_slice(Ctx* c, uint32_t mode, bool timing, bool ca
     if ((st = enqueue_restore(c)) != ASSE_OK) return st;
   }
   if (c->shard) {
-    if (c->sync_mode == 0 && (st = device_barrier(c)) != ASSE_OK) return st;   // all merged + published
+    if (c->sync_mode != 1 && (st = rank_barrier(c)) != ASSE_OK) return st;   // all merged + published
     if ((st = enqueue_gather(c)) != ASSE_OK) return st;
   }
   if ((st = enqueue_sort(c)) != ASSE_OK) return st;
@@ -1115,7 +1148,7 @@ static asse_status collect_enqueue(Ctx* c, uint32_t mode, uint32_t K, bool advan
   if (!c->ev_collect) CK(cudaEventCreateWithFlags(&c->ev_collect, cudaEventDisableTiming));
   CK(cudaEventRecord(c->ev_collect, s));
   if (advance) {
-    c->stats.kernel_launches += kEndSliceKernels + (c->peers && c->sync_mode == 0 ? 3 : 0) +
+    c->stats.kernel_launches += kEndSliceKernels + (c->peers && c->sync_mode == 0 ? 3 : 0) + (c->peers && c->sync_mode != 1 ? 1 : 0) +
                                 (c->sort_bound > kSortCap ? 8 : 0);   // prep, radix passes, gather, select
     c->stats.fold_launches++;
     c->t += 1;
@@ -1248,7 +1281,7 @@ static asse_status end_slice_enqueue(Ctx* c, uint32_t mode, uint32_t* K_out) {
   // graph is identical for every slice (host copies stay outside the graph)
   *c->h_clock = c->C0;
   CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
-  if ((c->peers && c->sync_mode == 0) || c->shard) {
+  if ((c->peers && c->sync_mode != 1) || c->shard) {
     asse_status st = enqueue_end_slice(c, mode, timing, false);   // epochs / phases change per slice
     c->begun = false;
     if (st != ASSE_OK) return st;
@@ -1346,13 +1379,16 @@ asse_status asse_fetch_reports(void* ctx, asse_report* h_out, uint32_t cap, uint
 }
 
 // ------------------------------------------------------------ checkpoint
-// File: "ASSECKPT" | u32 version (2) | u32 code_bytes | u32 k, k', r, c, u, s, g, world, rank, shard | f64 theta |
-//       u64 seed | u64 t | u32 C0 | u32 pad | pool codes (n_at * code_bytes, canonical values)
+// File: "ASSECKPT" | u32 version (3) | u32 code_bytes | u32 k, k', r, c, u, s, g, world, rank, shard,
+//       mangle, pad | f64 theta | u64 seed | u64 t | u32 C0 | u32 pad | pool codes (n_at * code_bytes,
+//       canonical values). Version 3 adds mangle (the key A and the host -> ATV map depend on it).
+constexpr uint32_t kCkptVersion = 3;
 struct CkptHeader {
   char magic[8];
   uint32_t version, code_bytes;
   uint32_t k, kp, r, c, u, s, g;
   uint32_t world, rank, shard;
+  uint32_t mangle, pad0;
   double theta;
   uint64_t seed, t;
   uint32_t C0, pad1;
@@ -1365,8 +1401,8 @@ asse_status asse_save_state(void* ctx, const char* path) {
   CK(cudaSetDevice(c->device));
   CkptHeader h{};
   memcpy(h.magic, "ASSECKPT", 8);
-  h.version = 2; h.code_bytes = c->cb;
-  h.world = c->cfg.world; h.rank = c->cfg.rank; h.shard = c->shard ? 1 : 0;
+  h.version = kCkptVersion; h.code_bytes = c->cb;
+  h.world = c->cfg.world; h.rank = c->cfg.rank; h.shard = c->shard ? 1 : 0; h.mangle = c->cfg.mangle;
   h.k = c->cfg.k; h.kp = c->kp; h.r = c->cfg.r; h.c = c->cfg.c; h.u = c->cfg.u; h.s = c->cfg.s;
   h.g = c->cfg.g; h.theta = c->cfg.theta; h.seed = c->cfg.seed; h.t = c->t; h.C0 = c->C0;
   std::vector<uint8_t> buf(c->n_at * c->cb);
@@ -1390,7 +1426,13 @@ asse_status asse_load_state(void* ctx, const char* path) {
   CkptHeader h{};
   std::vector<uint8_t> buf(c->n_at * c->cb);
   bool ok = fread(&h, sizeof(h), 1, f) == 1;
-  if (ok && (memcmp(h.magic, "ASSECKPT", 8) != 0 || h.version != 2)) { fclose(f); c->err = "not an ASSE checkpoint (v2)"; return ASSE_E_PARAM; }
+  if (ok && (memcmp(h.magic, "ASSECKPT", 8) != 0 || h.version != kCkptVersion)) {
+    fclose(f); c->err = "not an ASSE checkpoint (version 3)"; return ASSE_E_PARAM;
+  }
+  if (ok && h.mangle != c->cfg.mangle) { fclose(f); c->err = "checkpoint mangling (mangle) differs"; return ASSE_E_PARAM; }
+  if (ok && (h.C0 != (uint32_t)(h.t % c->two_k) || (c->cfg.n_slices && h.t > c->cfg.n_slices))) {
+    fclose(f); c->err = "checkpoint clock inconsistent: C0 != t mod 2k, or t beyond n_slices"; return ASSE_E_PARAM;
+  }
   if (ok && h.shard != (c->shard ? 1u : 0u)) { fclose(f); c->err = "checkpoint frame sharding differs"; return ASSE_E_PARAM; }
   if (ok && h.shard && (h.world != c->cfg.world || h.rank != c->cfg.rank)) {
     fclose(f); c->err = "frame-sharded checkpoint of another rank/world"; return ASSE_E_PARAM;
@@ -1463,6 +1505,88 @@ asse_status asse_get_stats(const void* ctx, asse_stats* out) {
 
 void* asse_get_stream(const void* ctx) {
   return ctx ? (void*)static_cast<const Ctx*>(ctx)->stream : nullptr;
+}
+
+asse_status asse_set_host_barrier(void* ctx, asse_host_barrier_fn fn, void* arg) {
+  if (!ctx) return ASSE_E_PARAM;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  c->host_barrier = fn;
+  c->host_barrier_arg = arg;
+  return ASSE_OK;
+}
+
+// ------------------------------------------------------------ CUDA IPC helpers
+static_assert(sizeof(cudaIpcMemHandle_t) == ASSE_IPC_HANDLE_BYTES, "IPC handle size");
+
+asse_status asse_ipc_alloc(int32_t device, uint64_t bytes, void** d_ptr, uint8_t* handle) {
+  if (!d_ptr || !handle || bytes == 0) return ASSE_E_PARAM;
+  *d_ptr = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return ASSE_E_CUDA;
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return ASSE_E_CUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+    cudaFree(p);
+    return ASSE_E_CUDA;
+  }
+  memcpy(handle, &h, sizeof(h));
+  *d_ptr = p;
+  return ASSE_OK;
+}
+
+asse_status asse_ipc_open(const uint8_t* handle, int32_t device, void** d_ptr) {
+  if (!d_ptr || !handle) return ASSE_E_PARAM;
+  *d_ptr = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return ASSE_E_CUDA;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  if (cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return ASSE_E_PEER;
+  }
+  return ASSE_OK;
+}
+
+asse_status asse_ipc_free(void* d_ptr, int32_t opened) {
+  if (!d_ptr) return ASSE_OK;
+  cudaError_t e = opened ? cudaIpcCloseMemHandle(d_ptr) : cudaFree(d_ptr);
+  return e == cudaSuccess ? ASSE_OK : ASSE_E_CUDA;
+}
+
+// Self-test of the device barrier (k_barrier's protocol) as ONE cooperative kernel whose
+// blocks play the ranks: never as separate launches that wait on each other.
+asse_status asse_selftest_barrier(int32_t device, uint32_t world, uint32_t epochs, uint64_t* errors) {
+  if (!errors || world < 2 || world > (uint32_t)kMaxWorld || epochs == 0) return ASSE_E_PARAM;
+  *errors = ~0ull;
+  if (cudaSetDevice(device) != cudaSuccess) return ASSE_E_CUDA;
+  uint32_t* mem = nullptr;
+  const size_t pad_words = 64, words = (size_t)world * pad_words + (size_t)world * 32 + 2;
+  if (cudaMalloc(&mem, words * 4) != cudaSuccess) return ASSE_E_CUDA;
+  asse_status st = ASSE_OK;
+  do {
+    if (cudaMemset(mem, 0, words * 4) != cudaSuccess) { st = ASSE_E_CUDA; break; }
+    BarrierTestParams tp{};
+    for (uint32_t w = 0; w < world; ++w) tp.bp.pads[w] = mem + w * pad_words;
+    tp.bp.world = world;
+    tp.data = mem + world * pad_words;
+    tp.errors = reinterpret_cast<unsigned long long*>(mem + world * pad_words + world * 32);
+    tp.epochs = epochs;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(world);
+    cfg.blockDim = dim3(32);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_barrier_selftest, tp) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) { cudaGetLastError(); st = ASSE_E_CUDA; break; }
+    unsigned long long e = 0;
+    if (cudaMemcpy(&e, tp.errors, 8, cudaMemcpyDeviceToHost) != cudaSuccess) { st = ASSE_E_CUDA; break; }
+    *errors = e;
+  } while (0);
+  cudaFree(mem);
+  return st;
 }
 
 }  // extern "C"

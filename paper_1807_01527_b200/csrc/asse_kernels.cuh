@@ -1012,24 +1012,52 @@ struct BarrierParams {
   uint32_t world, rank, epoch;
 };
 
-// Stream-ordered cross-GPU barrier: publish `epoch` into slot [rank] of every
-// peer's pad (release, system scope), then wait until every slot of our pad
-// reached `epoch` (acquire). One process per GPU only (never several ranks on one GPU).
-__global__ void k_barrier(BarrierParams p) {
+// Cross-rank barrier over signal pads: publish `epoch` into slot [rank] of every peer's
+// pad (release, system scope), then wait until every slot of our pad reached `epoch`
+// (acquire). Called by one whole block of >= world threads.
+__device__ __forceinline__ void barrier_ranks(uint32_t* const* pads, uint32_t world, uint32_t rank,
+                                              uint32_t epoch) {
   const uint32_t w = threadIdx.x;
-  if (w < p.world) {
-    uint32_t* dst = p.pads[w] + p.rank;
-    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(dst), "r"(p.epoch) : "memory");
-  }
   __syncthreads();
-  if (w < p.world) {
-    const uint32_t* src = p.pads[p.rank] + w;
+  if (w < world) {
+    uint32_t* dst = pads[w] + rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(dst), "r"(epoch) : "memory");
+  }
+  if (w < world) {
+    const uint32_t* src = pads[rank] + w;
     uint32_t v;
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(src) : "memory");
-    } while ((int32_t)(v - p.epoch) < 0);
+    } while ((int32_t)(v - epoch) < 0);
   }
   __syncthreads();
+}
+
+// Stream-ordered cross-GPU barrier (sync_mode 0). One process per GPU only: never launch
+// several ranks' barriers on one GPU (nothing guarantees they run at the same time).
+__global__ void k_barrier(BarrierParams p) { barrier_ranks(p.pads, p.world, p.rank, p.epoch); }
+
+// asse_selftest_barrier: the ranks are the blocks of ONE cooperative launch (co-resident).
+// Per epoch e every rank writes data[rank] = e, crosses the barrier, checks that it sees
+// data[w] == e for every w (the release/acquire chain), and crosses a second barrier before
+// the next epoch overwrites the data (reads ordered before the peers' next writes).
+struct BarrierTestParams {
+  BarrierParams bp;
+  uint32_t* data;                  // [world] x 32 words
+  unsigned long long* errors;
+  uint32_t epochs;
+};
+__global__ void k_barrier_selftest(BarrierTestParams p) {
+  const uint32_t rank = blockIdx.x, w = threadIdx.x;
+  for (uint32_t e = 1; e <= p.epochs; ++e) {
+    if (w == 0) p.data[rank * 32] = e;
+    barrier_ranks(p.bp.pads, p.bp.world, rank, 2 * e - 1);
+    if (w < p.bp.world) {
+      const uint32_t v = *reinterpret_cast<volatile uint32_t*>(p.data + w * 32);
+      if (v != e) atomicAdd(p.errors, 1ull);
+    }
+    barrier_ranks(p.bp.pads, p.bp.world, rank, 2 * e);
+  }
 }
 
 }  // namespace asse

@@ -79,15 +79,26 @@ __device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t* p) {
   asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
-__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// Poll a monotone counter (relaxed: the data it guards is read with L2-coherent .cg loads
-// issued after the poll returns; the writer published it with a release fence).
+// Release-add on a monotone counter: every memory access of this thread (and, through the
+// preceding bar.sync, of its group) is ordered before the increment (PTX memory model).
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+// Poll a monotone counter with acquire loads. The queue protocol's ordering chain (PTX
+// memory model, gpu scope):
+//   producer: queue stores / overflow REDs -> mbarrier arrive -> signal warp's wait
+//             -> fence (__threadfence, cumulative) -> atomicAdd(prod_done)
+//   owner:    acquire poll of prod_done -> bar.sync -> .cg loads of the entries; the final
+//             write-back of the owned slice follows the acquire of every round's count
+//   owner:    entry loads -> bar.sync -> red.release add(cons_done)
+//   producer: acquire poll of cons_done -> bar.sync -> stores into the reused ring range
 __device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t target, uint32_t ns = 128) {
-  while (ld_relaxed_gpu(p) < target) __nanosleep(ns);   // polls must not steal issue slots
+  while (ld_acquire_gpu(p) < target) __nanosleep(ns);   // polls must not steal issue slots
 }
 // mbarrier wait for warps off the critical path (sleeps between probes)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, uint32_t ns) {
@@ -288,7 +299,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
       // early so its latency hides behind the binning
       uint32_t seen = 0;
       const uint32_t need = G * (t / kBinNB);
-      if (tid == 0 && t >= (uint32_t)kBinNB && t < R) seen = ld_relaxed_gpu(cons_done + (t % kBinNB) * kBinPad);
+      if (tid == 0 && t >= (uint32_t)kBinNB && t < R) seen = ld_acquire_gpu(cons_done + (t % kBinNB) * kBinPad);
       if (t < R) {
         const uint64_t tile = (uint64_t)t * G + me;
         if (tile < n_tiles) {
@@ -414,7 +425,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
           }
       }
       named_bar(2 + grp, kGroupThreads);
-      if (gtid == 0) atomicAdd(cons_done + b * kBinPad, 1u);   // entries consumed (values used) before
+      if (gtid == 0) red_release_add(cons_done + b * kBinPad, 1u);   // entries consumed (values used) before
       c1 = clock64(); cwork += c1 - c0; c0 = c1;
     }
     if (bp.prof && gtid == 0) { bp.prof[me * 16 + 9 + 2 * grp] = cwait; bp.prof[me * 16 + 10 + 2 * grp] = cwork; }

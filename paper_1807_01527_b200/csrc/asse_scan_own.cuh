@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       c1 = clock64(); pc[1] += c1 - c0; c0 = c1;
       uint32_t seen = 0;
       const uint32_t need = O * (t / kOwnNB);    // owners that drained round t - NB
-      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R) seen = ld_relaxed_gpu(cons_done + (t % kOwnNB) * kBinPad);
+      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R) seen = ld_acquire_gpu(cons_done + (t % kOwnNB) * kBinPad);
       const uint64_t tile = (uint64_t)t * G + me;
       if (t < R && tile < n_tiles) {
         const uint32_t st = i % nst;
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       }
       named_bar(2 + grp, kGroupThreads);
       if (gtid == 0) {
-        atomicAdd(cons_done + b * kBinPad, 1u);  // entries consumed before
+        red_release_add(cons_done + b * kBinPad, 1u);   // entries consumed before
 #pragma unroll
         for (int g = 0; g < (int)kOwnQG; ++g) slast[b][g] = en[g];
       }

@@ -3,8 +3,10 @@
 Packets of a slice are split round-robin across ranks: slot j goes to rank
 j mod D (BASELINE.json.configs[4]). Every rank scans its shard into a local
 per-slice touch bitmap; at end_slice the bitmaps are OR-merged over NVLink peer
-memory (k_merge_or, csrc/asse_kernels.cu) so every rank folds the same global
-touches into an identical replicated AT pool (A26 combine rule).
+memory (k_merge_or / k_merge_shard, csrc/asse_kernels.cuh; A26 combine rule).
+Peer setup: attach_symmetric_peers (torch symmetric memory, device barrier,
+sync_mode 0), IpcPeers (CUDA IPC handles over the process group, host barrier,
+sync_mode 2) or attach_local_peers (virtual ranks in one process, sync_mode 1).
 """
 
 
@@ -60,3 +62,53 @@ def attach_local_peers(ctxs):
     for c in ctxs:
         c.attach_peers(tp, mp, None, xp, sync_mode=1)
     return touch, merged, xchg
+
+
+class IpcPeers:
+    """Peer buffers shared by CUDA IPC (one process per rank on one node) with the host
+    barrier of sync_mode 2 (asse_set_host_barrier -> torch.distributed.barrier). Ranks may
+    share a GPU: no kernel waits on another rank's kernel. Keep the object alive as long
+    as the context; close() unmaps and frees the buffers."""
+
+    def __init__(self, ctx, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        from paper_1807_01527_b200 import asse
+
+        group = group or dist.group.WORLD
+        self.group = group
+        dev = torch.cuda.current_device() if device is None else device
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        shard = bool(ctx.cfg.frame_shard)
+        sizes = [ctx.bitmap_bytes(), ctx.merged_bytes()] + ([ctx.exchange_bytes()] if shard else [])
+        self.own, self.opened, ptrs = [], [], []
+        for size in sizes:
+            p, h = asse.ipc_alloc(size, dev)
+            self.own.append(p)
+            handles = [None] * world
+            dist.all_gather_object(handles, h, group=group)
+            row = []
+            for w in range(world):
+                if w == rank:
+                    row.append(p)
+                else:
+                    q = asse.ipc_open(handles[w], dev)
+                    self.opened.append(q)
+                    row.append(q)
+            ptrs.append(row)
+        dist.barrier(group)
+        ctx.set_host_barrier(lambda: dist.barrier(group))
+        ctx.attach_peers(ptrs[0], ptrs[1], None, ptrs[2] if shard else None, sync_mode=2)
+        self.ptrs = ptrs
+
+    def close(self):
+        """Collective: unmap the peers' buffers, wait for every rank to do the same, then
+        free this rank's own (the context using them must be destroyed first)."""
+        import torch.distributed as dist
+        from paper_1807_01527_b200 import asse
+        for q in self.opened:
+            asse.ipc_free(q, True)
+        dist.barrier(self.group)
+        for p in self.own:
+            asse.ipc_free(p, False)
+        self.opened, self.own = [], []

@@ -126,3 +126,59 @@ def test_async_end_slice_pipeline(cuda_device, name, N, T, variant):
         dev.end_slice_wait()
     compare_pool(dev.pool(), ora.pool(), "%s async pool" % name)
     assert dev.clock()[0] == T
+
+
+def test_checkpoint_rejects_mangle_and_clock_mismatch(cuda_device, tmp_path):
+    """Version-3 header: a pool saved with mangle = 0 is refused by a mangle = 1 context
+    (A8: the key A and the host -> ATV map differ), and a header whose C0 is not
+    t mod 2k is refused."""
+    import struct
+    p = dict(PRESETS["C1"])
+    a = asse.Asse(**p)
+    g = Generator("C1")
+    for t in range(2):
+        d, ptr = to_device(g.slice(t))
+        a.scan_slice(ptr, g.N)
+        a.end_slice()
+    path = str(tmp_path / "c1.ckpt")
+    a.save_state(path)
+    with pytest.raises(asse.AsseError) as e:
+        asse.Asse(**dict(p, mangle=1)).load_state(path)
+    assert e.value.status == asse.E_PARAM and "mangl" in str(e.value)
+    raw = bytearray(open(path, "rb").read())
+    assert raw[:8] == b"ASSECKPT" and struct.unpack_from("<I", raw, 8)[0] == 3
+    # header: magic 8 | version, code_bytes | k, kp, r, c, u, s, g | world, rank, shard |
+    # mangle, pad | theta | seed | t | C0
+    off_c0 = 8 + 4 * 2 + 4 * 7 + 4 * 3 + 4 * 2 + 8 + 8 + 8
+    assert struct.unpack_from("<I", raw, off_c0)[0] == a.clock()[1] == 2
+    struct.pack_into("<I", raw, off_c0, 3)
+    bad = str(tmp_path / "bad.ckpt")
+    open(bad, "wb").write(bytes(raw))
+    with pytest.raises(asse.AsseError) as e:
+        asse.Asse(**p).load_state(bad)
+    assert e.value.status == asse.E_PARAM
+
+
+@pytest.mark.parametrize("variant", [1, 3])
+def test_side_stream_scan_after_async_end_slice(cuda_device, variant):
+    """A scan issued on a caller stream right after asse_end_slice_async must run after
+    that slice's fold (which reads and clears the touch bitmap): slice by slice equal to
+    the oracle (the caller stream now waits for the context stream)."""
+    p = dict(PRESETS["C3"])
+    dev, ora = asse.Asse(**p), O.Oracle(**p)
+    dev.set_scan_variant(variant)
+    side = torch.cuda.Stream()
+    g = Generator("C3", N=3_000_000)
+    live, expect = [], None
+    for t in range(4):
+        pk = g.slice(t)
+        d, ptr = to_device(pk)
+        live = (live + [d])[-2:]
+        dev.scan_slice(ptr, len(pk), stream=side.cuda_stream)
+        ora.scan(pk)
+        if t:
+            compare_reports(dev.end_slice_wait(), expect, p["theta"], "side t=%d" % (t - 1))
+        dev.end_slice_async(1)
+        expect = ora.end_slice(1)
+    compare_reports(dev.end_slice_wait(), expect, p["theta"], "side last")
+    compare_pool(dev.pool(), ora.pool(), "side pool")
