@@ -43,14 +43,40 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic():
-    """dram bytes per k_scan launch from the committed ncu --set full summary, if any."""
+def load_kernel_traffic():
+    """Per-kernel counters of the committed ncu --set full capture (tools/ncu_summary.py ->
+    profiles/kernel_traffic.json): DRAM bytes, L2 hit rate, shared-memory wavefronts."""
     try:
-        with open(os.path.join(ROOT, "profiles", "scan_traffic.json")) as f:
-            d = json.load(f)
-        return d
+        with open(os.path.join(ROOT, "profiles", "kernel_traffic.json")) as f:
+            return json.load(f)
     except Exception:
         return None
+
+
+def host_cpu():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+class PinnedToOneCore:
+    """taskset-equivalent: the oracle timing runs pinned to one core."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.cpu = sorted(self.old)[-1]
+        os.sched_setaffinity(0, {self.cpu})
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.old)
 
 
 def load_l2_peak():
@@ -132,20 +158,21 @@ class ClockSampler:
         return out
 
 
-def oracle_sample(p, pk_host, n_slice, reps=1):
-    """Time the plain CPU oracle (one thread) on a bounded sample: scan `pk_host`
-    (a prefix of one slice) and close the slice at the full geometry; project the
-    per-slice time to the full slice of n_slice packets. Returns (Gpps, detail)."""
+def oracle_slice(p, pk_host):
+    """Time the plain CPU oracle (single-threaded C, pinned to one core) on one whole
+    slice: scan every packet of `pk_host` and close the slice at the full geometry.
+    Nothing is projected. Returns (Gpps, detail)."""
     from oracle import oracle as O
     o = O.Oracle(**p)
-    t0 = time.perf_counter()
-    o.scan(pk_host)
-    t1 = time.perf_counter()
-    o.end_slice(0)
-    t2 = time.perf_counter()
+    with PinnedToOneCore() as pin:
+        t0 = time.perf_counter()
+        o.scan(pk_host)
+        t1 = time.perf_counter()
+        o.end_slice(0)
+        t2 = time.perf_counter()
     scan_s, end_s = t1 - t0, t2 - t1
-    per_slice = scan_s * (n_slice / len(pk_host)) + end_s
-    return n_slice / per_slice / 1e9, dict(scan_s=scan_s, end_s=end_s, sample_packets=len(pk_host))
+    return len(pk_host) / (scan_s + end_s) / 1e9, dict(scan_s=scan_s, end_s=end_s,
+                                                       packets=len(pk_host), pinned_cpu=pin.cpu)
 
 
 def workload_config(args, p, n_slice, world, S=None):
@@ -164,36 +191,47 @@ def workload_config(args, p, n_slice, world, S=None):
 
 
 def bench_reference(args, p, n_slice):
-    """--impl reference: the CPU oracle as it stands, rank 0 only."""
+    """--impl reference: the CPU oracle as it stands, rank 0 only. Every timed step is one
+    WHOLE slice of the workload (all packets scanned, the slice closed at the full
+    geometry), timed as it runs — no projection. The untimed warm-up steps scan a 1M-packet
+    prefix only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from oracle import oracle as O
     gen = Generator(args.workload)
-    sample = args.ref_sample
     o = O.Oracle(**p)
-    step_s = []
-    for step in range(args.warmup + args.steps):
-        pk = gen.slice(step, n=sample, threads=os.cpu_count())
-        t0 = time.perf_counter()
-        o.scan(pk)
-        t1 = time.perf_counter()
-        o.end_slice(0)
-        t2 = time.perf_counter()
-        if step >= args.warmup:
-            step_s.append((t1 - t0) * (n_slice / sample) + (t2 - t1))
+    step_s, scan_s, end_s = [], [], []
+    with PinnedToOneCore() as pin:
+        for step in range(args.warmup + args.steps):
+            timed = step >= args.warmup
+            os.sched_setaffinity(0, pin.old)            # generation uses every core
+            pk = gen.slice(step, n=None if timed else min(n_slice, 1_000_000), threads=os.cpu_count())
+            os.sched_setaffinity(0, {pin.cpu})
+            t0 = time.perf_counter()
+            o.scan(pk)
+            t1 = time.perf_counter()
+            o.end_slice(0)
+            t2 = time.perf_counter()
+            if timed:
+                step_s.append(t2 - t0)
+                scan_s.append(t1 - t0)
+                end_s.append(t2 - t1)
     total = sum(step_s)
     value = n_slice * args.steps / total / 1e9
+    cpu = dict(host_cpu(), value=value, unit="Gpps", cores=1, kind="oracle", pinned_cpu=pin.cpu,
+               extrapolated=False,
+               sample="every timed step: one whole slice of %s (%d packets scanned + end_slice at the "
+                      "full geometry), single-threaded C oracle pinned to one core; mean scan %.2f s, "
+                      "end_slice %.2f s per slice" % (args.workload, n_slice, statistics.mean(scan_s),
+                                                      statistics.mean(end_s)))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gpps",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u16", "data": "synthetic",
         "config": workload_config(args, p, n_slice, args.gpus),
-        "cpu_baseline": {"value": value, "unit": "Gpps", "cores": 1, "kind": "oracle",
-                         "sample": "per step: first %d packets of slice t scanned, full end_slice "
-                                   "at the full geometry; scan time projected to %d packets"
-                                   % (sample, n_slice)},
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "Gpps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -208,8 +246,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C5", choices=sorted(PRESETS))
     ap.add_argument("--distinct", type=int, default=8, help="distinct pre-generated slices")
-    ap.add_argument("--ref-sample", type=int, default=2_000_000)
-    ap.add_argument("--cpu-sample", type=int, default=20_000_000)
+    ap.add_argument("--slice-log", default=None,
+                    help="write one JSON line per slice of the instrumented pass (t, packets, scan / "
+                         "end_slice device ms, phases, |CSIP|, reports, super ATVs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--scan-variant", type=int, default=0, choices=[0, 1, 2, 3],
@@ -313,10 +352,33 @@ def main():
         end_ms.append(s["last_end_slice_ms"])
         for k in phases:
             phases[k].append(s[k])
+    slice_log = open(args.slice_log, "w") if (args.slice_log and rank == 0) else None
     sa = ctx.stats()
     t_inst = args.warmup + args.steps
     n_inst = args.steps
-    run(t_inst, t_inst + n_inst, record)
+    if slice_log:
+        # per-slice metrics log: one JSON line per closed slice
+        prev = dict(sa)
+        t_next = [t_inst]
+
+        def record_and_log(rep):
+            nonlocal prev
+            record(rep)
+            s = ctx.stats()
+            slice_log.write(json.dumps({
+                "t": t_next[0], "packets": n_slice, "packets_this_rank": n_local,
+                "scan_ms_harvested": s["scan_ms_total"] - prev["scan_ms_total"],
+                "end_slice_ms": s["last_end_slice_ms"], "fold_ms": s["last_fold_ms"],
+                "restore_nat_sort_ms": s["last_restore_ms"], "merge_ms": s["last_merge_ms"],
+                "csip": s["last_n_candidates"], "reports_above_theta": len(rep),
+                "super_atvs": s["last_n_super"], "scan_kernel_launches": s["scan_launches"] - prev["scan_launches"]})
+                + "\n")
+            prev = dict(s)
+            t_next[0] += 1
+        run(t_inst, t_inst + n_inst, record_and_log)
+        slice_log.close()
+    else:
+        run(t_inst, t_inst + n_inst, record)
     sb = ctx.stats()
     ctx.set_timing(False)
     scan_launch_ms = (sb["scan_ms_total"] - sa["scan_ms_total"]) / max(1, sb["scan_launches"] - sa["scan_launches"])
@@ -329,11 +391,22 @@ def main():
     peak, peak_src = load_peaks()
     scan_bytes = n_local * (8 + p["r"] * cb)          # 8 B read + r codes written
     scan_gbs = scan_bytes / (scan_launch_ms / 1e3) / 1e9
-    traffic = load_traffic()
-    n_at = p["r"] * (1 << p["u"]) * (1 << p["c"]) * p["g"]
+    kt = load_kernel_traffic()
+    ktk = (kt or {}).get("kernels", {})
+    scan_ncu = ktk.get(scan_kernel)
+    n_at = p["r"] * (1 << p["u"]) * (1 << p["c"]) * p["g"] // (world if shard else 1)
     bm = n_at // 8
-    fold_bytes = 2 * n_at * cb + 3 * bm                # pool read+write, touch read+clear, active write
-    fold_gbs = fold_bytes / (fold_launch_ms / 1e3) / 1e9
+    pool_b = n_at * cb
+    # SURVEY §8(d) end_slice algorithmic bytes: pool read + touch bitmap + sweep writes (2 of
+    # the 2k blocks per slice, i.e. pool / k); the SetATs' code writes are charged to the scan
+    fold_bytes_8d = pool_b + bm + pool_b // p["k"]
+    fold_gbs_8d = fold_bytes_8d / (fold_launch_ms / 1e3) / 1e9
+    # this design's own traffic: the scan writes 1-bit touches, so the fold writes every code
+    # back (pool read + write), reads the touches and writes the active bits (touch clear and
+    # active write stay in L2 in practice, see ncu)
+    fold_bytes_design = 2 * pool_b + 2 * bm
+    fold_gbs_design = fold_bytes_design / (fold_launch_ms / 1e3) / 1e9
+    fold_ncu = ktk.get("k_fold")
 
     # ---- e2e: host buffers through the public API (H2D inside the timed region)
     e2e = None
@@ -383,16 +456,16 @@ def main():
         gen.slice_cuda(1 % S, dst.data_ptr(), j0=j0, n=n_local, stride=stride)
         torch.cuda.synchronize()
 
-    # ---- cpu baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+    # ---- cpu baseline: the oracle on one whole slice (rank 0, N = 1 only; ~10-20 s of CPU)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        m = min(args.cpu_sample, n_local)
-        pk = bufs[0][: 2 * m].cpu().numpy().view(np.uint32).reshape(-1, 2)
-        v, det = oracle_sample(p, pk, n_slice)
-        cpu = {"value": v, "unit": "Gpps", "cores": 1, "kind": "oracle",
-               "sample": "slice 0 of %s: first %d packets scanned (%.1f s) + full end_slice at "
-                         "the full geometry (%.1f s), scan projected to %d packets/slice"
-                         % (args.workload, m, det["scan_s"], det["end_s"], n_slice)}
+        pk = bufs[0].cpu().numpy().view(np.uint32).reshape(-1, 2)
+        v, det = oracle_slice(p, pk)
+        cpu = dict(host_cpu(), value=v, unit="Gpps", cores=1, kind="oracle", pinned_cpu=det["pinned_cpu"],
+                   extrapolated=False,
+                   sample="slice 0 of %s: all %d packets scanned (%.1f s) + end_slice at the full geometry "
+                          "(%.1f s), single-threaded C oracle pinned to one core"
+                          % (args.workload, det["packets"], det["scan_s"], det["end_s"]))
 
     if rank == 0:
         line = {
@@ -411,13 +484,25 @@ def main():
             "gpu_launches": launches,
             "roofline": {"kernel": scan_kernel, "bound": "hbm", "achieved": scan_gbs, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": scan_gbs / peak,
-                         "traffic": (traffic["dram_bytes_per_packet"] * n_local)
-                         if traffic and traffic.get("kernel", "k_scan") == scan_kernel else None,
+                         "traffic": (scan_ncu["dram_bytes"] * n_local / kt["packets_per_scan_launch"])
+                         if scan_ncu and "dram_bytes" in scan_ncu else None,
                          "algorithmic_bytes_per_launch": scan_bytes,
                          "avg_launch_ms": scan_launch_ms,
+                         # random-access evidence (north_star): the scan's scattered SetATs, where
+                         # they land (L2 hit rate, L2 sector throughput, shared-memory wavefronts)
+                         "l2_hit_rate_pct": scan_ncu.get("l2_hit_rate_pct") if scan_ncu else None,
+                         "lts_throughput_pct": scan_ncu.get("lts_throughput_pct") if scan_ncu else None,
+                         "l1_shared_pipe_pct": scan_ncu.get("l1_shared_pipe_pct") if scan_ncu else None,
+                         "shared_wavefronts_per_packet": (scan_ncu["shared_wavefronts"] / kt["packets_per_scan_launch"])
+                         if scan_ncu and "shared_wavefronts" in scan_ncu else None,
+                         "shared_atom_wavefronts_per_packet": (scan_ncu["shared_atom_wavefronts"]
+                                                               / kt["packets_per_scan_launch"])
+                         if scan_ncu and "shared_atom_wavefronts" in scan_ncu else None,
+                         "ncu_source": (kt or {}).get("source"),
                          "note": "algorithmic bytes = 8 B read + r*code_bytes written per packet (SURVEY "
                                  "8(d)); the SetATs never reach HBM (1-bit touches in L2 / shared memory), "
-                                 "so the scan is bound on chip, see set_at_updates"},
+                                 "so the scan is bound on chip, see set_at_updates; traffic and the ncu "
+                                 "fields come from the committed ncu capture (profiles/kernel_traffic.json)"},
             "set_at_updates": {"kernel": scan_kernel,
                                "achieved": p["r"] * n_local / (scan_launch_ms / 1e3) / 1e9,
                                "unit": "G SetAT/s",
@@ -438,8 +523,17 @@ def main():
                                        "lifts the SetAT rate above the ceiling; k_scan_own: each packet "
                                        "travels once to the CTA owning (frame, word group of BH(bip)), which "
                                        "applies its r SetATs in shared memory"},
-            "kernels": {"k_fold": {"avg_launch_ms": fold_launch_ms, "algorithmic_bytes": fold_bytes,
-                                   "achieved_gbs": fold_gbs, "frac": fold_gbs / peak}},
+            "kernels": {"k_fold": {
+                "avg_launch_ms": fold_launch_ms,
+                "algorithmic_bytes": fold_bytes_8d, "achieved_gbs": fold_gbs_8d, "frac": fold_gbs_8d / peak,
+                "algorithmic_note": "SURVEY 8(d) end_slice bytes: pool read + touch bitmap + sweep writes "
+                                    "(pool / k); the codes of the slice's SetATs are charged to the scan",
+                "design_bytes": fold_bytes_design, "design_gbs": fold_gbs_design,
+                "design_frac": fold_gbs_design / peak,
+                "design_note": "this design's own traffic: the scan records 1-bit touches, so the fold "
+                               "reads and rewrites every code (2 x pool) plus touch read + active write",
+                "ncu_dram_bytes": fold_ncu.get("dram_bytes") if fold_ncu else None,
+                "ncu_l2_hit_rate_pct": fold_ncu.get("l2_hit_rate_pct") if fold_ncu else None}},
             "cpu_baseline": cpu,
             "reports_per_step": n_rep / args.steps,
         }

@@ -25,6 +25,18 @@ def build(force=False, verbose=False):
     return LIB
 
 
+def build_variant(out_path, defines=(), verbose=False):
+    """Build libasse with extra -D defines into out_path (tools/sweep.py). Never touches
+    the product library."""
+    cmd = [NVCC, *FLAGS, "-shared", "-I", os.path.join(ROOT, "include"),
+           *["-D" + d for d in defines], os.path.join(PKG, "csrc", "asse_api.cu"), "-o", out_path + ".tmp"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.check_call(cmd)
+    os.replace(out_path + ".tmp", out_path)
+    return out_path
+
+
 if __name__ == "__main__":
     import sys
     print(build(force=True, verbose="-v" in sys.argv))

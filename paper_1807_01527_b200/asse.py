@@ -71,11 +71,14 @@ HOST_BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
 IPC_HANDLE_BYTES = 64
 
 
-def load_library(path=LIB_PATH):
-    """Load libasse.so (raises if it is missing — there is no fallback)."""
+def load_library(path=None):
+    """Load libasse.so (raises if it is missing — there is no fallback). ASSE_LIB may name
+    another build of the same library (tools/sweep.py: kernel variants built out of tree,
+    never copied over the product .so)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("ASSE_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError("libasse.so not built (%s); run __graft_entry__.build()" % path)
     L = ctypes.CDLL(path)

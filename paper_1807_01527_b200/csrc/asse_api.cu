@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "asse.h"
 #include "asse_kernels.cuh"
 #include "asse_scan_bin.cuh"
@@ -22,6 +24,13 @@
 using namespace asse;
 
 namespace {
+
+// NVTX ranges around every public entry point that enqueues device work (tracing: nsys /
+// ncu --nvtx show the library's phases on the timeline; no-ops without a tool attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct AboveTheta {
   __host__ __device__ __forceinline__ bool operator()(const ReportDev& r) const {
@@ -63,6 +72,9 @@ struct Ctx {
   uint2* own_queue = nullptr;         // [NB][O][QG][QCAP]
   uint32_t* own_sync = nullptr;
   cudaStream_t stream = nullptr, copy_stream = nullptr;
+  cudaStream_t d2h_stream = nullptr;  // result copies of end_slice (off the context stream)
+  cudaEvent_t ev_done = nullptr;      // end of a slice's kernels on the context stream
+  bool collect_pending = false;       // ev_collect recorded: the next end_slice waits on it
   void* pool = nullptr;
   uint32_t* touch_own = nullptr;
   uint32_t* touch = nullptr;        // where k_scan records (own or peer-mapped)
@@ -199,6 +211,8 @@ static void free_all(Ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->d2h_stream) cudaStreamSynchronize(c->d2h_stream);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   void* dev[] = {c->pool, c->touch_own, c->active, c->scratch, c->sa_list, c->ws, c->cand, c->rep, c->rep_sorted, c->rep_above, c->keys,
                  c->keys_alt, c->vals, c->vals_alt, c->cub_tmp, c->export_buf, c->stage[0],
                  c->stage[1], c->bin_queue, c->bin_sync, c->own_queue, c->own_sync};
@@ -220,6 +234,9 @@ static void free_all(Ctx* c) {
   for (auto e : c->ev_free) cudaEventDestroy(e);
   for (auto e : c->ev) if (e) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->ev_collect) cudaEventDestroy(c->ev_collect);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -740,6 +757,9 @@ asse_status asse_init(const asse_config* cfg, void** out) {
     c->fold_grid = std::max(1, occ) * c->sms;
   }
   CKI(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  CKI(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+  CKI(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+  CKI(cudaEventCreateWithFlags(&c->ev_collect, cudaEventDisableTiming));
   const uint64_t bm_bytes = c->n_atv * c->wpa * 4;            // local (active, merged)
   const uint64_t touch_bytes = c->n_atv_full * c->wpa * 4;     // whole geometry
   CKI(cudaMalloc(&c->pool, c->n_at * c->cb));
@@ -866,6 +886,7 @@ asse_status asse_set_scan_variant(void* ctx, int variant) {
 static bool closed_all(const Ctx* c) { return c->cfg.n_slices && c->t >= c->cfg.n_slices; }
 
 asse_status asse_scan_slice(void* ctx, const uint32_t* d_pairs, uint64_t n_pairs, void* stream) {
+  NvtxRange nvtx_("asse_scan_slice");
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   if (closed_all(c)) { c->err = "all n_slices closed"; return ASSE_E_STATE; }
@@ -888,6 +909,7 @@ asse_status asse_scan_slice(void* ctx, const uint32_t* d_pairs, uint64_t n_pairs
 }
 
 asse_status asse_scan_slice_host(void* ctx, const uint32_t* h_pairs, uint64_t n_pairs) {
+  NvtxRange nvtx_("asse_scan_slice_host");
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   if (closed_all(c)) { c->err = "all n_slices closed"; return ASSE_E_STATE; }
@@ -968,6 +990,7 @@ uint64_t asse_exchange_bytes(const void* ctx) {
 }
 
 asse_status asse_merge(void* ctx) {
+  NvtxRange nvtx_("asse_merge");
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   NOT_PENDING(c);
@@ -1023,6 +1046,7 @@ static asse_status enqueue_gather(Ctx* c) {
   gp.rep = c->rep; gp.keys = c->keys; gp.vals = c->vals; gp.counters = c->counters;
   k_gather_peers<<<(unsigned)c->sms, 256, 0, s>>>(gp);
   CK(cudaGetLastError());
+  LAUNCHED(c);
   return ASSE_OK;
 }
 static asse_status enqueue_sort(Ctx* c) {
@@ -1139,16 +1163,22 @@ static constexpr int kEndSliceKernels = 3;   // fold, restore (+NAT), sort
 // kernels; ev_collect marks their arrival. With advance the slice counts as closed here
 // (a9: t+1, C0; preserveAT for t+1 was applied by k_fold, Alg. 2), so the next slice's
 // scans may be issued before the results are read.
+// The copies run on their own stream (d2h_stream), so the next slice's scan, queued on the
+// context stream behind this slice's kernels, does not wait for them; the next end_slice
+// waits for them (ev_collect) before its kernels overwrite the counters and reports.
 static asse_status collect_enqueue(Ctx* c, uint32_t mode, uint32_t K, bool advance) {
-  cudaStream_t s = c->stream;
-  CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, s));
+  cudaStream_t s = c->stream, d = c->d2h_stream;
+  CK(cudaEventRecord(c->ev_done, s));
+  CK(cudaStreamWaitEvent(d, c->ev_done, 0));
+  CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, d));
   CK(cudaMemcpyAsync(c->h_rep, mode ? c->rep_sorted : c->rep_above, (size_t)K * sizeof(ReportDev),
-                     cudaMemcpyDeviceToHost, s));
-  if (c->timing && advance) CK(cudaEventRecord(c->ev[9], s));
-  if (!c->ev_collect) CK(cudaEventCreateWithFlags(&c->ev_collect, cudaEventDisableTiming));
-  CK(cudaEventRecord(c->ev_collect, s));
+                     cudaMemcpyDeviceToHost, d));
+  if (c->timing && advance) CK(cudaEventRecord(c->ev[9], d));
+  CK(cudaEventRecord(c->ev_collect, d));
+  c->collect_pending = true;
   if (advance) {
-    c->stats.kernel_launches += kEndSliceKernels + (c->peers && c->sync_mode == 0 ? 3 : 0) + (c->peers && c->sync_mode != 1 ? 1 : 0) +
+    // merge / barrier / gather kernels of the eager multi-rank path count themselves
+    c->stats.kernel_launches += kEndSliceKernels +
                                 (c->sort_bound > kSortCap ? 8 : 0);   // prep, radix passes, gather, select
     c->stats.fold_launches++;
     c->t += 1;
@@ -1234,6 +1264,7 @@ static asse_status collect(Ctx* c, uint32_t mode, uint32_t K, asse_report* h_out
 }
 
 asse_status asse_end_slice_begin(void* ctx) {
+  NvtxRange nvtx_("asse_end_slice_begin");
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   NOT_PENDING(c);
@@ -1244,6 +1275,7 @@ asse_status asse_end_slice_begin(void* ctx) {
   if (closed_all(c)) { c->err = "all n_slices closed"; return ASSE_E_STATE; }
   CK(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
+  if (c->collect_pending) CK(cudaStreamWaitEvent(s, c->ev_collect, 0));
   *c->h_clock = c->C0;
   CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(c->xchg, 0, 64, s));
@@ -1268,7 +1300,7 @@ static asse_status end_slice_enqueue(Ctx* c, uint32_t mode, uint32_t* K_out) {
   const bool timing = c->timing;
   // report prefix copied with the counters: enough for the last slice's count + 25 %, so a
   // stable workload never needs a second copy (and synchronisation)
-  uint64_t want = std::max<uint64_t>(4096, (uint64_t)(mode ? c->last_n : c->last_above) * 5 / 4 + 64);
+  uint64_t want = std::max<uint64_t>(1024, (uint64_t)(mode ? c->last_n : c->last_above) * 5 / 4 + 64);
   want = std::min<uint64_t>(want, p.max_candidates);
   if (want > c->h_rep_cap) {
     if (c->h_rep) CK(cudaFreeHost(c->h_rep));
@@ -1277,6 +1309,9 @@ static asse_status end_slice_enqueue(Ctx* c, uint32_t mode, uint32_t* K_out) {
     CK(cudaMallocHost(&c->h_rep, c->h_rep_cap * sizeof(ReportDev)));
   }
   const uint32_t K = (uint32_t)std::min<uint64_t>(want, c->h_rep_cap);
+  // the previous slice's result copies (d2h_stream) finish before this slice's kernels
+  // rewrite the counters and report arrays
+  if (c->collect_pending) CK(cudaStreamWaitEvent(s, c->ev_collect, 0));
   // the per-slice ACT base reaches the kernels through device memory, so the captured
   // graph is identical for every slice (host copies stay outside the graph)
   *c->h_clock = c->C0;
@@ -1304,6 +1339,7 @@ static asse_status end_slice_enqueue(Ctx* c, uint32_t mode, uint32_t* K_out) {
 }
 
 asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out, uint32_t mode) {
+  NvtxRange nvtx_("asse_end_slice");
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   if (n_out) *n_out = 0;
@@ -1315,6 +1351,7 @@ asse_status asse_end_slice(void* ctx, asse_report* h_out, uint32_t cap, uint32_t
 }
 
 asse_status asse_end_slice_async(void* ctx, uint32_t mode) {
+  NvtxRange nvtx_("asse_end_slice_async");
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   NOT_PENDING(c);
@@ -1328,6 +1365,7 @@ asse_status asse_end_slice_async(void* ctx, uint32_t mode) {
 }
 
 asse_status asse_end_slice_wait(void* ctx, asse_report* h_out, uint32_t cap, uint32_t* n_out) {
+  NvtxRange nvtx_("asse_end_slice_wait");
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   if (n_out) *n_out = 0;
@@ -1343,6 +1381,7 @@ asse_status asse_end_slice_wait(void* ctx, asse_report* h_out, uint32_t cap, uin
 // of the advance only erased ages >= k-1 of that slice, which no k' < k window uses.
 asse_status asse_query_window(void* ctx, uint32_t k_prime, asse_report* h_out, uint32_t cap,
                               uint32_t* n_out, uint32_t mode) {
+  NvtxRange nvtx_("asse_query_window");
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   NOT_PENDING(c);
@@ -1355,6 +1394,7 @@ asse_status asse_query_window(void* ctx, uint32_t k_prime, asse_report* h_out, u
   const asse_config& p = c->cfg;
   cudaStream_t s = c->stream;
   const uint32_t K = (uint32_t)std::min<uint64_t>(c->h_rep_cap, p.max_candidates);
+  if (c->collect_pending) CK(cudaStreamWaitEvent(s, c->ev_collect, 0));
   *c->h_clock = (c->C0 + c->two_k - 1) % c->two_k;          // ACT base of the last closed slice
   CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, s));
@@ -1395,6 +1435,7 @@ struct CkptHeader {
 };
 
 asse_status asse_save_state(void* ctx, const char* path) {
+  NvtxRange nvtx_("asse_save_state");
   if (!ctx || !path) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   NOT_PENDING(c);
@@ -1417,6 +1458,7 @@ asse_status asse_save_state(void* ctx, const char* path) {
 }
 
 asse_status asse_load_state(void* ctx, const char* path) {
+  NvtxRange nvtx_("asse_load_state");
   if (!ctx || !path) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   NOT_PENDING(c);
@@ -1461,6 +1503,7 @@ uint64_t asse_pool_size(const void* ctx) {
 }
 
 asse_status asse_export_pool(void* ctx, uint16_t* h_out, uint64_t n) {
+  NvtxRange nvtx_("asse_export_pool");
   if (!ctx) return ASSE_E_PARAM;
   Ctx* c = static_cast<Ctx*>(ctx);
   NOT_PENDING(c);

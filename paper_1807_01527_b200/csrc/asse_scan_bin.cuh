@@ -86,8 +86,15 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 }
 // Release-add on a monotone counter: every memory access of this thread (and, through the
 // preceding bar.sync, of its group) is ordered before the increment (PTX memory model).
+#ifndef ASSE_REL_MODE
+#define ASSE_REL_MODE 0
+#endif
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+#if ASSE_REL_MODE == 0
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+#else   // tools only: the round-1 relaxed add (no release; measurement of the fence's cost)
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+#endif
 }
 // Poll a monotone counter with acquire loads. The queue protocol's ordering chain (PTX
 // memory model, gpu scope):
@@ -97,8 +104,49 @@ __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
 //             write-back of the owned slice follows the acquire of every round's count
 //   owner:    entry loads -> bar.sync -> red.release add(cons_done)
 //   producer: acquire poll of cons_done -> bar.sync -> stores into the reused ring range
+#ifndef ASSE_ACQ_MODE
+#define ASSE_ACQ_MODE 2
+#endif
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// How a wait acquires (measured at C5 on B200, tools/sweep.py r02c/r02d):
+//  0: every poll is an acquire load (LDG.STRONG + CCTL.IVALL per poll): scan 0.760 ms
+//  1: relaxed polls, then fence.acq_rel.gpu (MEMBAR.SC per wait): 0.870 ms
+//  2 (default): relaxed polls, then ONE acquire load of the counter once the target is
+//     seen — it reads a value >= target, i.e. the writer's release (fence + atomic add) or
+//     a later add of the same counter, so it synchronises with every round it counts
+__device__ __forceinline__ uint32_t ld_probe_gpu(const uint32_t* p) {
+#if ASSE_ACQ_MODE == 0
+  return ld_acquire_gpu(p);
+#else
+  return ld_relaxed_gpu(p);
+#endif
+}
 __device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t target, uint32_t ns = 128) {
+#if ASSE_ACQ_MODE == 0
   while (ld_acquire_gpu(p) < target) __nanosleep(ns);   // polls must not steal issue slots
+#elif ASSE_ACQ_MODE == 1
+  while (ld_relaxed_gpu(p) < target) __nanosleep(ns);
+  fence_acq_rel_gpu();
+#elif ASSE_ACQ_MODE == 2
+  while (ld_relaxed_gpu(p) < target) __nanosleep(ns);
+  while (ld_acquire_gpu(p) < target) {}                  // returns at once (monotone counter)
+#else   // 3, tools only: the round-1 relaxed polls without acquire (measures the ordering's cost)
+  while (ld_relaxed_gpu(p) < target) __nanosleep(ns);
+#endif
+}
+// after an early probe `seen` of *p: wait until *p >= target with acquire semantics
+__device__ __forceinline__ void wait_seen(uint32_t seen, const uint32_t* p, uint32_t target, uint32_t ns = 128) {
+  if (seen < target) spin_until_geq(p, target, ns);
+#if ASSE_ACQ_MODE == 1
+  else fence_acq_rel_gpu();
+#elif ASSE_ACQ_MODE == 2
+  else spin_until_geq(p, target, ns);                    // one acquire load
+#endif
 }
 // mbarrier wait for warps off the critical path (sleeps between probes)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, uint32_t ns) {
@@ -299,7 +347,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
       // early so its latency hides behind the binning
       uint32_t seen = 0;
       const uint32_t need = G * (t / kBinNB);
-      if (tid == 0 && t >= (uint32_t)kBinNB && t < R) seen = ld_acquire_gpu(cons_done + (t % kBinNB) * kBinPad);
+      if (tid == 0 && t >= (uint32_t)kBinNB && t < R) seen = ld_probe_gpu(cons_done + (t % kBinNB) * kBinPad);
       if (t < R) {
         const uint64_t tile = (uint64_t)t * G + me;
         if (tile < n_tiles) {
@@ -360,8 +408,8 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
         __syncwarp();
         if (lane == 0) mbar_arrive(&sigbar[tf % kSig]);   // this warp wrote round tf (release.cta)
       }
-      if (tid == 0 && t >= (uint32_t)kBinNB && t < R && seen < need)
-        spin_until_geq(cons_done + (t % kBinNB) * kBinPad, need);   // round t-NB drained everywhere
+      if (tid == 0 && t >= (uint32_t)kBinNB && t < R)
+        wait_seen(seen, cons_done + (t % kBinNB) * kBinPad, need);   // round t-NB drained everywhere
       named_bar(1, kBinT);                       // bins of round t final; staging sf and counts reusable
       c1 = clock64(); pc[2] += c1 - c0; c0 = c1;
     }

@@ -179,6 +179,37 @@ __device__ __forceinline__ void own_apply(const OwnScanParams& op, uint32_t* sbm
   }
 }
 
+#ifndef ASSE_OWN_CHECK
+#define ASSE_OWN_CHECK 0
+#endif
+// Owner-side SetAT of two entries with a read-before-atomic filter: the 2 x r words are
+// loaded first (plain shared loads, all independent), and only the rows whose touch bit is
+// still clear take an atomicOr. Exact: touch bits only go from 0 to 1 during a scan, so a
+// set bit seen by the load is set (a stale 0 only costs an unneeded atomic). A repeated
+// <aip, bip> pair — most packets of a busy slice — then costs r loads and no atomic.
+template <class Geo>
+__device__ __forceinline__ void own_apply2_check(const OwnScanParams& op, uint32_t* sbm, uint4 x) {
+  uint32_t w[8], m[8], cur[8];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const uint32_t e = q ? x.z : x.x, mk = q ? x.w : x.y;
+    const uint64_t L = (uint64_t)(e >> Geo::u(op));
+    const uint64_t D = L | (L << Geo::W(op));
+    const uint32_t sub = e & Geo::fmask(op);
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const uint32_t xc = (uint32_t)(D >> Geo::shift(op, y)) & Geo::cmask(op);
+      w[4 * q + y] = (((((uint32_t)y << Geo::c(op)) | xc) << Geo::lg_wg(op)) | sub);
+      m[4 * q + y] = mk;                           // 0 for a padding entry
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) cur[k] = sbm[w[k]];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (m[k] & ~cur[k]) atomicOr(sbm + w[k], m[k]);
+}
+
 // Bin two packets: f(aip), BH(bip), owner, one slot atomic each, one 8-byte store each.
 // The entry carries what the owner needs and nothing it knows: the LBS L in the
 // high 32-u bits, the word within the owner's group (< 2^u, host-checked) in the frame
@@ -309,7 +340,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       c1 = clock64(); pc[1] += c1 - c0; c0 = c1;
       uint32_t seen = 0;
       const uint32_t need = O * (t / kOwnNB);    // owners that drained round t - NB
-      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R) seen = ld_acquire_gpu(cons_done + (t % kOwnNB) * kBinPad);
+      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R) seen = ld_probe_gpu(cons_done + (t % kOwnNB) * kBinPad);
       const uint64_t tile = (uint64_t)t * G + me;
       if (t < R && tile < n_tiles) {
         const uint32_t st = i % nst;
@@ -376,8 +407,8 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         __syncwarp();
         if (lane == 0) mbar_arrive(&sigbar[tf % kSig]);   // this warp wrote round tf
       }
-      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R && seen < need)
-        spin_until_geq(cons_done + (t % kOwnNB) * kBinPad, need, 128);   // round t-NB drained
+      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R)
+        wait_seen(seen, cons_done + (t % kOwnNB) * kBinPad, need, 128);   // round t-NB drained
       named_bar(1, kBinT);                       // bins of round t final; staging sf and counts reusable
       c1 = clock64(); pc[2] += c1 - c0; c0 = c1;
     }
@@ -427,8 +458,12 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint4 x = v[g][u];
+#if ASSE_OWN_CHECK
+            if (x.y | x.w) own_apply2_check<Geo>(op, sbm, x);
+#else
             if (x.y) own_apply<Geo>(op, sbm, x.x, x.y);
             if (x.w) own_apply<Geo>(op, sbm, x.z, x.w);
+#endif
           }
       }
       named_bar(2 + grp, kGroupThreads);

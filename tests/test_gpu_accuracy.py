@@ -72,6 +72,8 @@ def test_accuracy_c2(cuda_device):
     assert s["true_super_points"] > 100 and s["fnr"] < 0.5
 
 
-def test_accuracy_c3(cuda_device):
-    s, g = _run("C3", 64, 59)
+def test_accuracy_c3_reduced(cuda_device):
+    """C3 traffic at 5M packets/slice through its first full window (the BASELINE-size
+    C3/C4/C5 and g-sweep reports: tools/accuracy.py -> profiles/accuracy_r02.json)."""
+    s, g = _run("C3", 62, 59, N=5_000_000)
     assert s["true_super_points"] > 100 and s["fnr"] < 0.5

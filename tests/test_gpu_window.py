@@ -7,12 +7,13 @@ tests run the exact instantiations bench.py times past every one of those points
 compare the pool, CSIP, NAT and the estimates with the oracle after EVERY slice:
 
 * C3 geometry (u8 codes, g = 512, k = 60: k_fold<1,5>, k_scan_own<1,GeoC3> chosen by the
-  automatic rule at 3M packets/slice): 2k + 5 = 125 slices, so erasures start at t = 60
+  automatic rule at 2.6M packets/slice): 2k + 5 = 125 slices, so erasures start at t = 60
   and C0 wraps at t = 120.
 * C4 shape (u16 codes, g = 512 < 2k = 600: a = 0, every AT in block 2k-1, A7; k = 300:
-  k_fold<2,5>, the C4 instantiation), with c = 8, s = 7 to bound the oracle's time (the
-  fold's template and its per-AT clock logic do not depend on c; SURVEY/VERDICT allow
-  it): 2k + 5 = 605 slices of the C4 mixture with its on/off DDoS spans.
+  k_fold<2,5>, the C4 instantiation), with c = 9, s = 7 (completeness 9 + 3*7 >= 28, 8
+  duplicate positions) and 20k packets/slice to bound the oracle's time and keep the
+  smaller sketch below saturation (the fold's template and its per-AT clock logic do not
+  depend on c): 2k + 5 = 605 slices of the C4 mixture with its on/off DDoS spans.
 * C5 at full size (100M packets/slice) through the pipelined asse_end_slice_async the
   bench uses, 3 slices.
 
@@ -63,16 +64,16 @@ def test_full_window_c3_production_geometry(cuda_device):
     """k_scan_own (automatic choice) + k_fold<1,5> over 125 slices of C3 traffic."""
     p = dict(PRESETS["C3"])
     assert (p["k"], p["g"], p["c"], p["u"], p["s"]) == (60, 512, 12, 4, 6)
-    gen = Generator("C3", N=3_000_000)
+    gen = Generator("C3", N=2_600_000)
     st = _run_window(p, gen, 2 * p["k"] + 5, 0, "scan_own_launches", "C3 window")
     assert st["code_bytes"] == 1
 
 
 def test_full_window_c4_shape_u16(cuda_device):
     """k_fold<2,5> (u16, a = 0) over 605 slices of the C4 mixture (DDoS bursts on/off)."""
-    p = dict(PRESETS["C4"], c=8, s=7)
+    p = dict(PRESETS["C4"], c=9, s=7)
     assert (p["k"], p["g"]) == (300, 512)
-    gen = Generator("C4", N=200_000)
+    gen = Generator("C4", N=20_000)
     st = _run_window(p, gen, 2 * p["k"] + 5, 3, "scan_own_launches", "C4-shape window")
     assert st["code_bytes"] == 2
 

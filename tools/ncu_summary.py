@@ -116,6 +116,41 @@ def main():
                 json.dump({"source": "%s %s ncu --set full" % (a.tag, d["kernel"]), "kernel": kname,
                            "packets_per_launch": a.packets, "dram_bytes_per_launch": (mb + wb) * 1e6,
                            "dram_bytes_per_packet": per}, f, indent=1)
+    if a.report:
+        # per-kernel counters bench.py reports next to its live timings (roofline.traffic,
+        # the scan's random-access evidence, k_fold's DRAM bytes)
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        kt = {"source": "%s ncu --set full --clock-control none (one launch per kernel)" % a.tag,
+              "packets_per_scan_launch": a.packets, "kernels": {}}
+        for d in res:
+            short = d["kernel"].split("::")[-1].split("<")[0].split("(")[0].strip()
+            if short in kt["kernels"]:
+                continue
+            e = {"instantiation": d["kernel"]}
+            for key, m in (("dram_read_bytes", "dram__bytes_read.sum"), ("dram_write_bytes", "dram__bytes_write.sum")):
+                if m in d:
+                    v, u = d[m].split()[0], d[m].split()[1]
+                    e[key] = float(v.replace(",", "")) * scale[u]
+            for key, m in (("l2_hit_rate_pct", "lts__t_sector_hit_rate.pct"),
+                           ("lts_throughput_pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                           ("dram_throughput_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                           ("l1_shared_pipe_pct", "l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                           ("issue_pct", "sm__inst_issued.avg.pct_of_peak_sustained_active"),
+                           ("shared_wavefronts", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+                           ("shared_atom_wavefronts", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum"),
+                           ("shared_bank_conflicts", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+                           ("lts_sectors_read", "lts__t_sectors_op_read.sum"),
+                           ("lts_sectors_write", "lts__t_sectors_op_write.sum"),
+                           ("lts_sectors_red", "lts__t_sectors_op_red.sum"),
+                           ("inst_executed", "smsp__inst_executed.sum"),
+                           ("duration_us", "gpu__time_duration.sum")):
+                if m in d:
+                    e[key] = num(d[m])
+            if "dram_read_bytes" in e and "dram_write_bytes" in e:
+                e["dram_bytes"] = e["dram_read_bytes"] + e["dram_write_bytes"]
+            kt["kernels"][short] = e
+        with open(os.path.join(a.out, "kernel_traffic.json"), "w") as f:
+            json.dump(kt, f, indent=1)
     with open(os.path.join(a.out, "%s_ncu_summary.md" % a.tag), "w") as f:
         f.write("\n".join(md) + "\n")
     with open(os.path.join(a.out, "%s_ncu_summary.json" % a.tag), "w") as f:
