@@ -105,7 +105,7 @@ __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
 //   owner:    entry loads -> bar.sync -> red.release add(cons_done)
 //   producer: acquire poll of cons_done -> bar.sync -> stores into the reused ring range
 #ifndef ASSE_ACQ_MODE
-#define ASSE_ACQ_MODE 2
+#define ASSE_ACQ_MODE 0
 #endif
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   uint32_t v;
@@ -113,12 +113,16 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-// How a wait acquires (measured at C5 on B200, tools/sweep.py r02c/r02d):
-//  0: every poll is an acquire load (LDG.STRONG + CCTL.IVALL per poll): scan 0.760 ms
+// How a wait acquires (k_scan_own at C5 on B200, tools/sweep.py r02c/r02d; round 1's
+// relaxed polls without any acquire: 0.712 ms):
+//  0 (default): every poll is an acquire load (LDG.STRONG + CCTL.IVALL): 0.760 ms with the
+//     binning warps' own early probe; the acquire reads a value >= target, i.e. the
+//     writer's release (fence + atomic add) or a later add of the same counter, so it
+//     synchronises with every round it counts
 //  1: relaxed polls, then fence.acq_rel.gpu (MEMBAR.SC per wait): 0.870 ms
-//  2 (default): relaxed polls, then ONE acquire load of the counter once the target is
-//     seen — it reads a value >= target, i.e. the writer's release (fence + atomic add) or
-//     a later add of the same counter, so it synchronises with every round it counts
+//  2: relaxed polls, then one acquire load once the target is seen: 0.827 ms (one more
+//     serial L2 round trip per wait)
+// k_scan_own keeps every global acquire off its binning warps (signal-warp handoff).
 __device__ __forceinline__ uint32_t ld_probe_gpu(const uint32_t* p) {
 #if ASSE_ACQ_MODE == 0
   return ld_acquire_gpu(p);
@@ -135,6 +139,10 @@ __device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t targe
 #elif ASSE_ACQ_MODE == 2
   while (ld_relaxed_gpu(p) < target) __nanosleep(ns);
   while (ld_acquire_gpu(p) < target) {}                  // returns at once (monotone counter)
+#elif ASSE_ACQ_MODE == 4
+  if (ld_acquire_gpu(p) >= target) return;              // ready: one acquire load
+  while (ld_relaxed_gpu(p) < target) __nanosleep(ns);   // waiting: polls without CCTL.IVALL
+  while (ld_acquire_gpu(p) < target) {}
 #else   // 3, tools only: the round-1 relaxed polls without acquire (measures the ordering's cost)
   while (ld_relaxed_gpu(p) < target) __nanosleep(ns);
 #endif
