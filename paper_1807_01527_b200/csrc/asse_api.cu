@@ -382,7 +382,9 @@ static asse_status launch_scan_bin(Ctx* c, const uint2* pk, uint64_t n, const Sc
 template <int CB, bool MP, class Geo>
 static cudaError_t coop_launch_own(Ctx* c, const uint2* pk, uint64_t n, const OwnScanParams& op, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(c->bin_G);
+  // tools only: ASSE_OWN_GRID = CTAs of the packet-owned scan (>= owners; default one per SM)
+  static const uint32_t grid_env = getenv("ASSE_OWN_GRID") ? (uint32_t)atoi(getenv("ASSE_OWN_GRID")) : 0u;
+  cfg.gridDim = dim3(grid_env >= c->own_O && grid_env <= c->bin_G ? grid_env : c->bin_G);
   cfg.blockDim = dim3(kOwnThreads);
   cfg.dynamicSmemBytes = c->own_smem;
   cfg.stream = st;
@@ -733,7 +735,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
         // ~16 entries per bin per round on average (CAP = 30): 2048 packets at O = 128
         c->own_tile = std::min<uint32_t>(2048u, std::max<uint32_t>(1024u, c->own_O * 16u) / 1024u * 1024u) * 8u;
         if (const char* e = getenv("ASSE_SCAN_TILE")) c->own_tile = ((uint32_t)atoi(e) + 255u) / 256u * 256u * 8u;
-        const uint64_t slice_words = (uint64_t)(p.r - kOwnRR) << (p.c + c->own_lg_wg);
+        const uint64_t slice_words = (uint64_t)p.r << (p.c + c->own_lg_wg);
         c->own_smem = own_smem_bytes(c->own_O, (uint32_t)std::min<uint64_t>(slice_words, 1u << 30), c->own_tile);
         c->own_ok = coop && p.r == 4 && (1u << lg_wpa) == c->wpa && c->own_O <= (uint32_t)c->sms && c->own_lg_wg <= p.u &&
                     c->own_O <= kOwnMaxOwners && c->own_O >= 2 &&

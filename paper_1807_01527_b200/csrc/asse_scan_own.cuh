@@ -50,9 +50,6 @@ namespace asse {
 #ifndef ASSE_OWN_NGR
 #define ASSE_OWN_NGR 4
 #endif
-#ifndef ASSE_OWN_X2
-#define ASSE_OWN_X2 0
-#endif
 #ifndef ASSE_OWN_U
 #define ASSE_OWN_U 1
 #endif
@@ -69,17 +66,13 @@ constexpr int kOwnConsWarps = ASSE_OWN_CONS_WARPS;         // queue-draining war
 constexpr int kOwnConsWarp0 = kOwnBinWarps;
 constexpr int kOwnTmaWarp = kOwnConsWarp0 + kOwnConsWarps;
 constexpr int kOwnSigWarp = kOwnTmaWarp + 1;
-#ifndef ASSE_OWN_FREEWARP
-#define ASSE_OWN_FREEWARP 3
-#endif
-// buffer-reuse handoff (global acquire, see the free loop below), measured at C5 (scan ms,
-// tools/sweep.py r02k-r02n; round 1's relaxed probes without acquire: 0.715):
-//  0 = the binning warps probe cons_done themselves with an acquire (it stalls the round): 0.754
-//  1 = a warp of its own (ptxas drops to 92 registers, the binning loop rematerialises): 0.755
-//  2 = lane 1 of the signal warp (independent thread scheduling interleaves it with lane 0): 0.750
-//  3 (default) = lane 1 of the TMA warp: 0.729
-constexpr int kOwnFreeWarp = (ASSE_OWN_FREEWARP == 1) ? kOwnSigWarp + 1 : -1;
-constexpr int kOwnThreads = 32 * (kOwnSigWarp + 1 + (ASSE_OWN_FREEWARP == 1 ? 1 : 0));
+// buffer-reuse handoff (the global acquire of cons_done, see the free loop below) runs in
+// lane 1 of the TMA warp. Alternatives measured at C5 (scan ms, tools/sweep.py r02k-r02n;
+// round 1's relaxed probes without any acquire: 0.715): the binning warps probing cons_done
+// with an acquire themselves 0.754 (the acquire stalls the round); a warp of its own 0.755
+// (ptxas drops to 92 registers and the binning loop rematerialises); lane 1 of the signal
+// warp 0.750; lane 1 of the TMA warp 0.729.
+constexpr int kOwnThreads = 32 * (kOwnSigWarp + 1);
 constexpr int kOwnRing = 2;                                // packet-tile ring stages
 constexpr uint32_t kOwnCap = 30;                           // staged entries per (owner, round) in a CTA; also
                                                            // the bin stride (240 B, 16-B aligned; bin o
@@ -103,13 +96,7 @@ constexpr uint32_t kOwnQG = ASSE_OWN_QG;                   // producer groups (C
 constexpr uint32_t kOwnQCap = ASSE_OWN_QCAP;
 static_assert((kOwnQCap & (kOwnQCap - 1)) == 0, "ring index is masked");                        // ring entries per (buffer, owner, group) >= the
                                                            // producer group's bins (host-checked)
-#ifndef ASSE_OWN_RR
-#define ASSE_OWN_RR 0
-#endif
-// rows applied by the producer as a global RED into the L2-resident touch bitmap (rows
-// 0 .. RR-1) instead of travelling to the owner: the L2's random-RED capacity then works
-// in parallel with the owners' shared-memory atomics (k_scan_bin's hybrid, §5.4)
-constexpr uint32_t kOwnRR = ASSE_OWN_RR;
+
 #ifndef OWN_FREE_SLEEP
 #define OWN_FREE_SLEEP 256
 #endif
@@ -191,43 +178,12 @@ __device__ __forceinline__ void own_apply(const OwnScanParams& op, uint32_t* sbm
   const uint64_t D = L | (L << Geo::W(op));
   const uint32_t sub = e & Geo::fmask(op);
 #pragma unroll
-  for (int y = kOwnRR; y < 4; ++y) {
+  for (int y = 0; y < 4; ++y) {
     const uint32_t x = (uint32_t)(D >> Geo::shift(op, y)) & Geo::cmask(op);
-    const uint32_t w = (((((uint32_t)(y - kOwnRR) << Geo::c(op)) | x) << Geo::lg_wg(op)) | sub);
-    OWN_ASSERT(w < ((uint32_t)(op.sp.r - kOwnRR) << (op.sp.c + op.lg_wg)) && m != 0u);
+    const uint32_t w = (((((uint32_t)y << Geo::c(op)) | x) << Geo::lg_wg(op)) | sub);
+    OWN_ASSERT(w < ((uint32_t)op.sp.r << (op.sp.c + op.lg_wg)) && m != 0u);
     atomicOr(sbm + w, m);
   }
-}
-
-#ifndef ASSE_OWN_CHECK
-#define ASSE_OWN_CHECK 0
-#endif
-// Owner-side SetAT of two entries with a read-before-atomic filter: the 2 x r words are
-// loaded first (plain shared loads, all independent), and only the rows whose touch bit is
-// still clear take an atomicOr. Exact: touch bits only go from 0 to 1 during a scan, so a
-// set bit seen by the load is set (a stale 0 only costs an unneeded atomic). A repeated
-// <aip, bip> pair — most packets of a busy slice — then costs r loads and no atomic.
-template <class Geo>
-__device__ __forceinline__ void own_apply2_check(const OwnScanParams& op, uint32_t* sbm, uint4 x) {
-  uint32_t w[8], m[8], cur[8];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const uint32_t e = q ? x.z : x.x, mk = q ? x.w : x.y;
-    const uint64_t L = (uint64_t)(e >> Geo::u(op));
-    const uint64_t D = L | (L << Geo::W(op));
-    const uint32_t sub = e & Geo::fmask(op);
-#pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      const uint32_t xc = (uint32_t)(D >> Geo::shift(op, y)) & Geo::cmask(op);
-      w[4 * q + y] = (((((uint32_t)(y < (int)kOwnRR ? 0 : y - kOwnRR) << Geo::c(op)) | xc) << Geo::lg_wg(op)) | sub);
-      m[4 * q + y] = y < (int)kOwnRR ? 0u : mk;    // 0 for a padding entry or a RED row
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) cur[k] = sbm[w[k]];
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-    if (m[k] & ~cur[k]) atomicOr(sbm + w[k], m[k]);
 }
 
 // Bin two packets: f(aip), BH(bip), owner, one slot atomic each, one 8-byte store each.
@@ -251,18 +207,6 @@ __device__ __forceinline__ void own_bin_two(const OwnScanParams& op, const uint4
   OWN_ASSERT(!valid || (o0 < op.O && o1 < op.O));
   const uint32_t pos0 = atoms_inc(valid ? scount_s + 4u * o0 : scount_dummy);
   const uint32_t pos1 = atoms_inc(valid ? scount_s + 4u * o1 : scount_dummy);
-  if (kOwnRR) {                                   // rows < RR: RED into the global bitmap (L2)
-    const uint32_t fcw = Geo::c(op) + Geo::u(op);
-#pragma unroll
-    for (int y = 0; y < (int)kOwnRR; ++y) {
-      const uint32_t xa = (uint32_t)(((uint64_t)(h0 >> Geo::u(op)) | ((uint64_t)(h0 >> Geo::u(op)) << Geo::W(op))) >> Geo::shift(op, y)) & Geo::cmask(op);
-      const uint32_t xb = (uint32_t)(((uint64_t)(h1 >> Geo::u(op)) | ((uint64_t)(h1 >> Geo::u(op)) << Geo::W(op))) >> Geo::shift(op, y)) & Geo::cmask(op);
-      const uint32_t atv0 = ((uint32_t)y << fcw) | ((h0 & fm) << Geo::c(op)) | xa;
-      const uint32_t atv1 = ((uint32_t)y << fcw) | ((h1 & fm) << Geo::c(op)) | xb;
-      red_or_if(valid, p.touch + (size_t)atv0 * (Geo::g(op) >> 5) + (i0 >> 5), 1u << touch_bit<CB>(i0));
-      red_or_if(valid, p.touch + (size_t)atv1 * (Geo::g(op) >> 5) + (i1 >> 5), 1u << touch_bit<CB>(i1));
-    }
-  }
   const bool ok0 = pos0 < cap, ok1 = pos1 < cap;
   sts64_if(valid && ok0, stg_s + 8u * (o0 * cap + pos0), (h0 & ~fm) | ((i0 >> 5) & wgm), 1u << touch_bit<CB>(i0));
   sts64_if(valid && ok1, stg_s + 8u * (o1 * cap + pos1), (h1 & ~fm) | ((i1 >> 5) & wgm), 1u << touch_bit<CB>(i1));
@@ -290,7 +234,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   uint2* stg = reinterpret_cast<uint2*>(smem + (size_t)nst * kTileBytes);             // [2][O][cap]
   uint32_t* scount = reinterpret_cast<uint32_t*>(stg + 2 * (size_t)O * cap);          // [2][Op]
   uint32_t* sbm = scount + 2 * Op + 4;           // 4 spare words: dummy bin counter (owners: the slice)
-  const uint32_t slice_words = (uint32_t)(op.sp.r - kOwnRR) << (op.sp.c + op.lg_wg);
+  const uint32_t slice_words = (uint32_t)op.sp.r << (op.sp.c + op.lg_wg);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint32_t head = (((uintptr_t)pk) & 15u) ? 1u : 0u;
   const uint64_t nbody = (n > head) ? n - head : 0;
@@ -318,7 +262,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   __syncthreads();
   const uint8_t* body = reinterpret_cast<const uint8_t*>(pk + head);
 
-  if (warp == kOwnSigWarp && !(ASSE_OWN_FREEWARP == 2 && lane == 1)) {   // ------ round publication
+  if (warp == kOwnSigWarp) {                     // ---------------- round publication
     if (lane == 0)
       for (uint32_t tf = 0; tf < R; ++tf) {
         mbar_wait_suspend(&sigbar[tf % kSig], (tf / kSig) & 1u);   // every binning warp wrote round tf
@@ -327,24 +271,23 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       }
     return;
   }
-  if ((int)warp == kOwnFreeWarp || (ASSE_OWN_FREEWARP == 2 && warp == kOwnSigWarp) ||
-      (ASSE_OWN_FREEWARP == 3 && warp == kOwnTmaWarp && lane == 1)) {   // --- buffer-reuse handoff
+  if (warp == kOwnTmaWarp && lane == 1) {       // ---------------- buffer-reuse handoff
     // the queue buffer of round t may be rewritten once every owner drained round t - NB:
-    // this warp acquires the owners' release adds (gpu scope) and hands the buffer to the
+    // this lane acquires the owners' release adds (gpu scope) and hands the buffer to the
     // binning warps through a CTA-scope mbarrier (release / acquire), so no binning thread
     // ever stalls on a global acquire load. Barrier t mod NB: its arrival for round t + NB
     // needs round t drained everywhere, i.e. published by this CTA's binning warps after
-    // they consumed the arrival for round t (no phase can be skipped).
-    if (lane == (ASSE_OWN_FREEWARP >= 2 ? 1u : 0u))
-      for (uint32_t t = kOwnNB; t < R; ++t) {
-        const uint32_t* cd = cons_done + (t % kOwnNB) * kBinPad;
-        const uint32_t need = O * (t / kOwnNB);
-        if (ld_acquire_gpu(cd) < need) {         // not yet: poll without the acquire's CCTL.IVALL
-          while (ld_relaxed_gpu(cd) < need) __nanosleep(OWN_FREE_SLEEP);
-          while (ld_acquire_gpu(cd) < need) {}
-        }
-        mbar_arrive(&freebar[t % kOwnNB]);
+    // they consumed the arrival for round t (no phase can be skipped). Lane 0 of this warp
+    // issues the tile copies; independent thread scheduling interleaves the two loops.
+    for (uint32_t t = kOwnNB; t < R; ++t) {
+      const uint32_t* cd = cons_done + (t % kOwnNB) * kBinPad;
+      const uint32_t need = O * (t / kOwnNB);
+      if (ld_acquire_gpu(cd) < need) {           // not yet: poll without the acquire's CCTL.IVALL
+        while (ld_relaxed_gpu(cd) < need) __nanosleep(OWN_FREE_SLEEP);
+        while (ld_acquire_gpu(cd) < need) {}
       }
+      mbar_arrive(&freebar[t % kOwnNB]);
+    }
     return;
   }
   if (warp == kOwnTmaWarp) {                     // ---------------- packet tiles -> ring
@@ -389,10 +332,6 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         OWN_ASSERT(cnt <= cap + 1u && (cnt & 1u) == 0u && (off & 1u) == 0u);
       }
       c1 = clock64(); pc[1] += c1 - c0; c0 = c1;
-#if !ASSE_OWN_FREEWARP
-      uint32_t seen = 0;
-      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R) seen = ld_probe_gpu(cons_done + (t % kOwnNB) * kBinPad);
-#endif
       const uint64_t tile = (uint64_t)t * G + me;
       if (t < R && tile < n_tiles) {
         const uint32_t st = i % nst;
@@ -405,22 +344,11 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         const uint4* tp = reinterpret_cast<const uint4*>(ring + (size_t)st * kTileBytes);
         const uint32_t stg_s = smem_u32(stg + (size_t)sb * O * cap), scount_s = smem_u32(scount + sb * Op);
         const uint32_t dummy_s = smem_u32(scount + 2 * Op);
-#if ASSE_OWN_X2
-        for (uint32_t q0 = tid - lane; q0 < n4; q0 += 2 * kBinT) {   // warp-uniform trip count
-          const uint32_t q = q0 + lane, q1 = q + kBinT;
-          const bool valid = q < n4, valid1 = q1 < n4;
-          const uint4 v0 = valid ? tp[q] : make_uint4(0, 0, 0, 0);
-          const uint4 v1 = valid1 ? tp[q1] : make_uint4(0, 0, 0, 0);
-          own_bin_two<CB, MP, Geo>(op, v0, valid, stg_s, scount_s, dummy_s);
-          own_bin_two<CB, MP, Geo>(op, v1, valid1, stg_s, scount_s, dummy_s);
-        }
-#else
         for (uint32_t q0 = tid - lane; q0 < n4; q0 += kBinT) {   // warp-uniform trip count
           const uint32_t q = q0 + lane;
           const bool valid = q < n4;
           own_bin_two<CB, MP, Geo>(op, valid ? tp[q] : make_uint4(0, 0, 0, 0), valid, stg_s, scount_s, dummy_s);
         }
-#endif
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
         ++i;
@@ -459,13 +387,8 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
         __syncwarp();
         if (lane == 0) mbar_arrive(&sigbar[tf % kSig]);   // this warp wrote round tf
       }
-#if ASSE_OWN_FREEWARP
-      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R)   // round t-NB drained (free loop)
+      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R)   // round t-NB drained (handoff lane)
         mbar_wait(&freebar[t % kOwnNB], ((t / kOwnNB) - 1u) & 1u);
-#else
-      if (tid == 0 && t >= (uint32_t)kOwnNB && t < R)   // round t-NB drained (early probe)
-        wait_seen(seen, cons_done + (t % kOwnNB) * kBinPad, O * (t / kOwnNB), 128);
-#endif
       named_bar(1, kBinT);                       // bins of round t final; staging sf and counts reusable
       c1 = clock64(); pc[2] += c1 - c0; c0 = c1;
     }
@@ -515,12 +438,8 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint4 x = v[g][u];
-#if ASSE_OWN_CHECK
-            if (x.y | x.w) own_apply2_check<Geo>(op, sbm, x);
-#else
             if (x.y) own_apply<Geo>(op, sbm, x.x, x.y);
             if (x.w) own_apply<Geo>(op, sbm, x.z, x.w);
-#endif
           }
       }
       named_bar(2 + grp, kGroupThreads);
@@ -555,7 +474,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       if (s.x | s.y) {
         const uint32_t w = q << 1;
         const uint32_t yx = w >> op.lg_wg, sub = w & (wg - 1u);
-        const uint32_t y = (yx >> p.c) + kOwnRR, x = yx & p.cmask;
+        const uint32_t y = yx >> p.c, x = yx & p.cmask;
         OWN_ASSERT((size_t)(y * row_words + x) * p.wpa + gbase + sub + 1 < (size_t)p.r * row_words * p.wpa);
         uint2* gd = reinterpret_cast<uint2*>(p.touch + (size_t)(y * row_words + x) * p.wpa + gbase + sub);
         uint2 gv;
@@ -568,7 +487,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
     for (uint32_t q = threadIdx.x; q < slice_words; q += kComputeThreads) {
       const uint32_t s = sbm[q];
       if (s) {
-        const uint32_t y = (q >> p.c) + kOwnRR, x = q & p.cmask;
+        const uint32_t y = q >> p.c, x = q & p.cmask;
         uint32_t* gd = p.touch + (size_t)(y * row_words + x) * p.wpa + gbase;
         *gd = ld_cg_u32(gd) | s;
       }
