@@ -187,6 +187,8 @@ def workload_config(args, p, n_slice, world, S=None):
            "l2": "inputs larger than L2 (%d MB per slice per GPU), no flush" % (8 * n_slice // world >> 20)}
     if S is not None:
         cfg["distinct_slices"] = S
+    if getattr(args, "peer_mode", None):
+        cfg["peers"] = args.peer_mode
     return cfg
 
 
@@ -291,7 +293,17 @@ def main():
     ctx = asse.Asse(**dict(p, world=world, rank=rank, device=local, max_candidates=1 << 20,
                            frame_shard=shard))
     ctx.set_scan_variant(args.scan_variant)
-    peers = attach_symmetric_peers(ctx) if world > 1 else None
+    peers, peer_mode = None, None
+    if world > 1:
+        try:                       # NVLink peer memory + device barrier (sync_mode 0)
+            peers = attach_symmetric_peers(ctx)
+            peer_mode = "symmetric memory, device barrier (sync_mode 0)"
+        except Exception as e:     # CUDA IPC + host barrier (sync_mode 2), tested on one GPU
+            from paper_1807_01527_b200.dist import IpcPeers
+            print("symmetric memory unavailable (%r): CUDA IPC peers, host barrier" % (e,), file=sys.stderr)
+            peers = IpcPeers(ctx)
+            peer_mode = "CUDA IPC, host barrier (sync_mode 2)"
+    args.peer_mode = peer_mode
     j0, stride, n_local = shard_slots(n_slice, rank, world)
 
     gen = Generator(args.workload)

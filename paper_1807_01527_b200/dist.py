@@ -30,6 +30,12 @@ def attach_symmetric_peers(ctx, group=None):
 
     group = group or dist.group.WORLD
     dev = torch.device("cuda", torch.cuda.current_device())
+    enable = getattr(symm_mem, "enable_symm_mem_for_group", None)
+    if enable is not None:
+        try:
+            enable(group.group_name)
+        except Exception:  # newer torch: no per-group opt-in needed
+            pass
     shard = bool(ctx.cfg.frame_shard)
     sizes = [ctx.bitmap_bytes(), ctx.merged_bytes(), 256] + ([ctx.exchange_bytes()] if shard else [])
     bufs, ptrs = [], []
