@@ -37,10 +37,12 @@ def test_query_window_equals_oracle_with_that_kprime(cuda_device, name, N):
     compare_pool(dev.pool(), oras[kps[-1]].pool(), "pool after queries")
 
 
-def test_checkpoint_roundtrip(cuda_device, tmp_path):
-    p = dict(PRESETS["C1"])
+@pytest.mark.parametrize("name", ["C1", "C4"])
+def test_checkpoint_roundtrip(cuda_device, tmp_path, name):
+    """u8 (C1) and u16 (C4, k = 300) pools: a resumed run equals the uninterrupted one."""
+    p = dict(PRESETS[name], N=200_000) if name == "C4" else dict(PRESETS[name])
     a = asse.Asse(**p)
-    g = Generator("C1")
+    g = Generator(name, N=p["N"])
     for t in range(3):
         d, ptr = to_device(g.slice(t))
         a.scan_slice(ptr, g.N)

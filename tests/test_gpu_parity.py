@@ -92,7 +92,7 @@ def test_long_run_sweeps_small_geometry(cuda_device):
         step_both(dev, ora, pk, geo["theta"], "long t=%d" % t, check_pool=(t % 7 == 0 or t in (299, 300, 301, 599, 600, 601)))
 
 
-@pytest.mark.parametrize("k,kp", [(1, 1), (4, 2), (10, 1), (60, 17), (100, 100)])
+@pytest.mark.parametrize("k,kp", [(1, 1), (4, 2), (10, 1), (60, 17), (100, 100), (600, 300)])
 def test_window_variants(cuda_device, k, kp):
     """discrete window k = 1, k' < k (Alg. 1), and u16 codes at k = 100."""
     geo = dict(k=k, k_prime=kp, r=4, c=10, u=4, s=6, g=256, theta=300.0, seed=9)
@@ -194,3 +194,4 @@ def test_state_machine_errors(cuda_device):
     assert e.value.status == asse.E_STATE
     with pytest.raises(asse.AsseError):
         asse.Asse(**dict(PRESETS["C1"], g=100))
+
