@@ -256,6 +256,13 @@ def main():
     ap.add_argument("--scan-variant", type=int, default=0, choices=[0, 1, 2, 3],
                     help="0 auto, 1 k_scan (direct RED.OR into L2), 2 k_scan_bin (shared-memory bins), "
                          "3 k_scan_own (packet-owned shared-memory slices)")
+    ap.add_argument("--peers", default="auto", choices=["auto", "symm", "ipc"],
+                    help="N>1 peer buffers: torch symmetric memory + device barrier (symm), CUDA IPC + "
+                         "host barrier (ipc), or symm with ipc as the fallback (auto)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--one-device", action="store_true",
+                    help="tests only: every rank on cuda:0 (CUDA IPC peers, host barriers, gloo); "
+                         "exercises the N>1 path on one GPU, its timings mean nothing")
     ap.add_argument("--replicated", action="store_true",
                     help="N>1: keep the whole pool on every GPU (option R) instead of frame sharding (S)")
     args = ap.parse_args()
@@ -273,10 +280,15 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit("WORLD_SIZE=%d but --gpus %d" % (world, args.gpus))
+    if args.one_device:          # tests only: every rank on cuda:0, CUDA IPC + host barriers
+        local, args.peers, args.dist_backend = 0, "ipc", "gloo"
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -285,7 +297,7 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if args.dist_backend == "nccl" else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
@@ -295,12 +307,19 @@ def main():
     ctx.set_scan_variant(args.scan_variant)
     peers, peer_mode = None, None
     if world > 1:
-        try:                       # NVLink peer memory + device barrier (sync_mode 0)
-            peers = attach_symmetric_peers(ctx)
-            peer_mode = "symmetric memory, device barrier (sync_mode 0)"
-        except Exception as e:     # CUDA IPC + host barrier (sync_mode 2), tested on one GPU
+        err = None
+        if args.peers in ("auto", "symm"):
+            try:                   # NVLink peer memory + device barrier (sync_mode 0)
+                peers = attach_symmetric_peers(ctx)
+                peer_mode = "symmetric memory, device barrier (sync_mode 0)"
+            except Exception as e:
+                if args.peers == "symm":
+                    raise
+                err = e
+        if peers is None:          # CUDA IPC + host barrier (sync_mode 2), tested on one GPU
             from paper_1807_01527_b200.dist import IpcPeers
-            print("symmetric memory unavailable (%r): CUDA IPC peers, host barrier" % (e,), file=sys.stderr)
+            if err is not None:
+                print("symmetric memory unavailable (%r): CUDA IPC peers, host barrier" % (err,), file=sys.stderr)
             peers = IpcPeers(ctx)
             peer_mode = "CUDA IPC, host barrier (sync_mode 2)"
     args.peer_mode = peer_mode

@@ -98,3 +98,28 @@ def test_device_barrier_protocol_cooperative(cuda_device, world):
     data of that epoch, and no rank overwrites data a peer has not read yet."""
     from paper_1807_01527_b200 import asse
     assert asse.selftest_barrier(world, 2000) == 0
+
+
+@pytest.mark.parametrize("extra", [[], ["--replicated"]])
+def test_bench_two_ranks_one_device(cuda_device, extra):
+    """bench.py's N>1 path (round-robin shards, frame-sharded or replicated pools, the
+    library's multi-rank end_slice, max-over-ranks timing, rank-0 JSON line) launched as the
+    driver launches it (torch.distributed.run), with both ranks on cuda:0 through CUDA IPC
+    peers and host barriers (--one-device). The numbers of such a run mean nothing."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "bench.py"), "--gpus", "2", "--one-device", "--workload", "C3",
+           "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu", "--distinct", "4"] + extra
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert "IPC" in d["config"]["peers"]
+    assert d["config"]["parallelism"].startswith("dp2")
+    assert d["reports_per_step"] > 0
