@@ -175,6 +175,26 @@ def oracle_slice(p, pk_host):
                                                        packets=len(pk_host), pinned_cpu=pin.cpu)
 
 
+def oracle_slice_all_cores(p, pk_host):
+    """Optional all-core variant (SURVEY §8(d) "Oracle timing"), reported separately from
+    the one-core baseline: the same slice scanned by the oracle's OpenMP loop (relaxed
+    atomic stores, the same pool as the serial scan, tests/test_oracle_scan_mt.py) on
+    every host core; end_slice stays the serial oracle."""
+    from oracle import oracle as O
+    o = O.Oracle(**p)
+    threads = O.lib().oracle_omp_threads()
+    t0 = time.perf_counter()
+    o.scan_mt(pk_host, 0)
+    t1 = time.perf_counter()
+    o.end_slice(0)
+    t2 = time.perf_counter()
+    scan_s, end_s = t1 - t0, t2 - t1
+    return dict(value=len(pk_host) / (scan_s + end_s) / 1e9, unit="Gpps", cores=threads, kind="oracle-openmp-scan",
+                scan_gpps=len(pk_host) / scan_s / 1e9,
+                sample="the same slice: scan on %d OpenMP threads (%.2f s), end_slice serial (%.2f s)"
+                       % (threads, scan_s, end_s))
+
+
 def workload_config(args, p, n_slice, world, S=None):
     """The `config` object of the JSON line (identical for both arms)."""
     cfg = {"workload": "%s: config-3 mixture, %d packets/slice split round-robin over %d GPU(s)"
@@ -497,6 +517,8 @@ def main():
                    sample="slice 0 of %s: all %d packets scanned (%.1f s) + end_slice at the full geometry "
                           "(%.1f s), single-threaded C oracle pinned to one core"
                           % (args.workload, det["packets"], det["scan_s"], det["end_s"]))
+        cpu["scan_only_gpps"] = det["packets"] / det["scan_s"] / 1e9
+        cpu["all_cores"] = oracle_slice_all_cores(p, pk)
 
     if rank == 0:
         line = {

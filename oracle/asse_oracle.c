@@ -29,6 +29,9 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define ORACLE_OK 0
 #define ORACLE_E_PARAM (-1)
@@ -339,6 +342,41 @@ void oracle_scan(oracle_t* o, const uint32_t* pairs, uint64_t n) {
     for (uint32_t y = 0; y < o->p.r; ++y)                  /* P:344 */
       oracle_touch(o, y, z, x[y], i);                      /* P:347 SetAT */
   }
+}
+
+/* The same Alg. 3 loop split over host threads — used ONLY by bench.py's optional
+ * all-core CPU baseline (SURVEY §8(d) "Oracle timing"), never for parity. Every SetAT of
+ * slice t writes the ACT of its block (P:185), a value fixed by (i, C0), so concurrent
+ * writers of one AT store the same value: relaxed atomic stores give the pool of
+ * oracle_scan exactly (pinned by tests/test_oracle_scan_mt.py). nthreads <= 0: every core. */
+void oracle_scan_mt(oracle_t* o, const uint32_t* pairs, uint64_t n, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+  {
+    uint32_t x[32], z;
+#pragma omp for schedule(static)
+    for (uint64_t q = 0; q < n; ++q) {
+      uint32_t aip = pairs[2 * q], bip = pairs[2 * q + 1];
+      oracle_digest(o, aip, &z, x);
+      uint32_t i = oracle_bh(o, bip);
+      uint16_t v = (uint16_t)oracle_act(o, i);
+      for (uint32_t y = 0; y < o->p.r; ++y)
+        __atomic_store_n(&o->pool[at_index(o, y, z, x[y], i)], v, __ATOMIC_RELAXED);
+    }
+  }
+#else
+  (void)nthreads;
+  oracle_scan(o, pairs, n);
+#endif
+}
+
+int oracle_omp_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
 }
 
 /* ------------------------------------------------------------- steps 2-6 */

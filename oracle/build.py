@@ -11,7 +11,7 @@ def build(force=False):
     if not force and os.path.exists(LIB) and all(
             os.path.getmtime(s) <= os.path.getmtime(LIB) for s in SRCS):
         return LIB
-    subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", *SRCS, "-lm", "-o", LIB])
+    subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", *SRCS, "-lm", "-o", LIB])
     return LIB
 
 

@@ -60,6 +60,8 @@ def lib():
             "oracle_pool_size": (u64, [vp]),
             "oracle_touch": (None, [vp, u32, u32, u32, u32]),
             "oracle_scan": (None, [vp, vp, u64]),
+            "oracle_scan_mt": (None, [vp, vp, u64, i32]),
+            "oracle_omp_threads": (i32, []),
             "oracle_nat": (u32, [vp, u32]),
             "oracle_detect": (i32, [vp]),
             "oracle_advance": (None, [vp]),
@@ -194,6 +196,11 @@ class Oracle:
     def scan(self, pairs):
         pairs = np.ascontiguousarray(pairs, dtype=np.uint32)
         lib().oracle_scan(self._h, pairs.ctypes.data, pairs.size // 2)
+
+    def scan_mt(self, pairs, nthreads=0):
+        """All-core variant of scan (bench.py's optional CPU baseline only; same pool)."""
+        pairs = np.ascontiguousarray(pairs, dtype=np.uint32)
+        lib().oracle_scan_mt(self._h, pairs.ctypes.data, pairs.size // 2, int(nthreads))
 
     def detect(self):
         return lib().oracle_detect(self._h)
