@@ -3,7 +3,6 @@
 // kernels; every step of the hot path runs in asse_kernels.cuh.
 //
 // P:n = PAPER.md line n; A<n> = reading n of DESIGN.md §2.
-#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -30,12 +29,6 @@ namespace {
 struct NvtxRange {
   explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
   ~NvtxRange() { nvtxRangePop(); }
-};
-
-struct AboveTheta {
-  __host__ __device__ __forceinline__ bool operator()(const ReportDev& r) const {
-    return (r.flags & 2u) != 0;
-  }
 };
 
 struct Ctx {
@@ -99,8 +92,7 @@ struct Ctx {
   ReportDev* rep_sorted = nullptr;
   ReportDev* rep_above = nullptr;
   uint32_t *keys = nullptr, *keys_alt = nullptr, *vals = nullptr, *vals_alt = nullptr;
-  void* cub_tmp = nullptr;
-  size_t cub_bytes = 0;
+  uint32_t* bs_buf = nullptr;       // bucket sort: [5][kBsMaxB] bucket arrays + [2][max_candidates]
   uint16_t* export_buf = nullptr;
   // host pinned
   uint32_t* h_counters = nullptr;
@@ -214,7 +206,7 @@ static void free_all(Ctx* c) {
   if (c->d2h_stream) cudaStreamSynchronize(c->d2h_stream);
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   void* dev[] = {c->pool, c->touch_own, c->active, c->scratch, c->sa_list, c->ws, c->cand, c->rep, c->rep_sorted, c->rep_above, c->keys,
-                 c->keys_alt, c->vals, c->vals_alt, c->cub_tmp, c->export_buf, c->stage[0],
+                 c->keys_alt, c->vals, c->vals_alt, c->bs_buf, c->export_buf, c->stage[0],
                  c->stage[1], c->bin_queue, c->bin_sync, c->own_queue, c->own_sync};
   for (void* p : dev) if (p) cudaFree(p);
   if (c->h_counters) cudaFreeHost(c->h_counters);
@@ -817,15 +809,7 @@ asse_status asse_init(const asse_config* cfg, void** out) {
   CKI(cudaMalloc(&c->keys_alt, (size_t)p.max_candidates * 4));
   CKI(cudaMalloc(&c->vals, (size_t)p.max_candidates * 4));
   CKI(cudaMalloc(&c->vals_alt, (size_t)p.max_candidates * 4));
-  {
-    size_t b1 = 0, b2 = 0;
-    cub::DoubleBuffer<uint32_t> dk(c->keys, c->keys_alt), dv(c->vals, c->vals_alt);
-    CKI(cub::DeviceRadixSort::SortPairs(nullptr, b1, dk, dv, (int)p.max_candidates, 0, 32, c->stream));
-    CKI(cub::DeviceSelect::If(nullptr, b2, c->rep_sorted, c->rep_above, c->counters + 4,
-                              (int)p.max_candidates, AboveTheta(), c->stream));
-    c->cub_bytes = std::max(b1, b2);
-    CKI(cudaMalloc(&c->cub_tmp, c->cub_bytes));
-  }
+  CKI(cudaMalloc(&c->bs_buf, (5ull * kBsMaxB + 2ull * p.max_candidates) * 4));
   CKI(cudaMallocHost(&c->h_counters, 64));
   CKI(cudaMallocHost(&c->h_clock, 64));
   CKI(cudaMalloc(&c->d_clock, 64));
@@ -1051,26 +1035,39 @@ static asse_status enqueue_gather(Ctx* c) {
   LAUNCHED(c);
   return ASSE_OK;
 }
+// Bucket sort of CSIP (k_bs_*, asse_kernels.cuh) for |CSIP| > kRankCap, |CSIP| read on the
+// device; `bound` (an expected |CSIP|) only sizes the buckets (~32 ips per bucket).
+static asse_status enqueue_bucket_sort(Ctx* c, const uint32_t* n_ptr, uint64_t bound, cudaStream_t s) {
+  uint32_t lgB = 6;
+  while (lgB < kBsMaxLgB && (1ull << lgB) * 32 < bound) ++lgB;
+  if (const char* e = getenv("ASSE_BS_LGB")) lgB = std::min<uint32_t>(kBsMaxLgB, std::max(1, atoi(e)));   // tests: crowded buckets
+  BucketSortParams bp{};
+  bp.rep = c->rep; bp.keys = c->keys; bp.vals = c->vals; bp.n_ptr = n_ptr;
+  bp.max_cand = c->cfg.max_candidates; bp.B = 1u << lgB; bp.shift = 32u - lgB;
+  bp.cnt = c->bs_buf; bp.off = bp.cnt + kBsMaxB; bp.cur = bp.off + kBsMaxB;
+  bp.acnt = bp.cur + kBsMaxB; bp.aoff = bp.acnt + kBsMaxB;
+  bp.arank = bp.aoff + kBsMaxB; bp.pbkt = bp.arank + c->cfg.max_candidates;
+  bp.tk = c->keys_alt; bp.tv = c->vals_alt;
+  bp.sorted = c->rep_sorted; bp.above = c->rep_above; bp.counters = c->counters;
+  const unsigned grid = (unsigned)c->sms * 4;
+  CK(cudaMemsetAsync(bp.cnt, 0, (size_t)bp.B * 4, s));
+  k_bs_count<<<grid, 256, 0, s>>>(bp);
+  k_bs_scan<<<1, 1024, 0, s>>>(bp);
+  k_bs_scatter<<<grid, 256, 0, s>>>(bp);
+  k_bs_bucket<<<(bp.B + kBsWarps - 1) / kBsWarps, 32 * kBsWarps, 0, s>>>(bp);
+  k_bs_scan2<<<1, 1024, 0, s>>>(bp);
+  k_bs_above<<<grid, 256, 0, s>>>(bp);
+  CK(cudaGetLastError());
+  return ASSE_OK;
+}
+
 static asse_status enqueue_sort(Ctx* c) {
   const uint32_t* n_ptr = c->counters + (c->shard ? 6 : 0);
   CK(launch_pdl(k_sort, dim3(kSortBlocks), dim3(kSortThreads), 0, c->stream, (const ReportDev*)c->rep,
                 c->counters, n_ptr, (uint32_t)c->cfg.max_candidates, c->rep_sorted, c->rep_above));
-  if (c->sort_bound > kSortCap) {
-    // |CSIP| beyond the block sort was seen: sort a bound of slots on the device (A24, A21)
-    cudaStream_t s = c->stream;
-    const uint32_t B = c->sort_bound, mc = c->cfg.max_candidates;
-    const unsigned blocks = (unsigned)std::min<uint64_t>((B + 255) / 256, (uint64_t)c->sms * 8);
-    k_sort_prep<<<blocks, 256, 0, s>>>(n_ptr, B, mc, c->keys, c->vals, c->counters);
-    CK(cudaGetLastError());
-    cub::DoubleBuffer<uint32_t> dk(c->keys, c->keys_alt), dv(c->vals, c->vals_alt);
-    size_t bytes = c->cub_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, dk, dv, (int)B, 0, 32, s));
-    k_gather_bound<<<blocks, 256, 0, s>>>(c->rep, dv.Current(), n_ptr, B, mc, c->rep_sorted);
-    CK(cudaGetLastError());
-    bytes = c->cub_bytes;
-    CK(cub::DeviceSelect::If(c->cub_tmp, bytes, c->rep_sorted, c->rep_above, c->counters + 4, (int)B,
-                             AboveTheta(), s));
-  }
+  // |CSIP| beyond the rank sort was seen: the bucket sort runs in the graph from then on
+  // (its kernels return at once while |CSIP| <= kRankCap)
+  if (c->sort_bound > kRankCap) return enqueue_bucket_sort(c, n_ptr, c->sort_bound, c->stream);
   return ASSE_OK;
 }
 
@@ -1181,7 +1178,7 @@ static asse_status collect_enqueue(Ctx* c, uint32_t mode, uint32_t K, bool advan
   if (advance) {
     // merge / barrier / gather kernels of the eager multi-rank path count themselves
     c->stats.kernel_launches += kEndSliceKernels +
-                                (c->sort_bound > kSortCap ? 8 : 0);   // prep, radix passes, gather, select
+                                (c->sort_bound > kRankCap ? kBsKernels : 0);   // the bucket sort
     c->stats.fold_launches++;
     c->t += 1;
     c->C0 = (uint32_t)(c->t % c->two_k);
@@ -1200,26 +1197,16 @@ static asse_status collect_finish(Ctx* c, uint32_t mode, uint32_t K, asse_report
   const uint32_t n_cand = overflow ? 0 : n_cand_raw;
   bool prefetched = true;
   if (!overflow && c->h_counters[5]) {
-    // |CSIP| above the block-sort capacity: device-wide radix sort (needs n on the host)
-    cub::DoubleBuffer<uint32_t> dk(c->keys, c->keys_alt), dv(c->vals, c->vals_alt);
-    size_t bytes = c->cub_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, dk, dv, (int)n_cand, 0, 32, s));
-    c->stats.kernel_launches += 4;  // onesweep radix passes (count is indicative)
-    unsigned blocks = (unsigned)std::min<uint64_t>((n_cand + 255) / 256, (uint64_t)c->sms * 8);
-    k_gather<<<blocks, 256, 0, s>>>(c->rep, dv.Current(), n_cand, c->rep_sorted);
-    CK(cudaGetLastError());
-    LAUNCHED(c);
-    bytes = c->cub_bytes;
-    CK(cub::DeviceSelect::If(c->cub_tmp, bytes, c->rep_sorted, c->rep_above, c->counters + 4,
-                             (int)n_cand, AboveTheta(), s));
-    c->stats.kernel_launches += 2;
+    // |CSIP| above the rank sort and the bucket sort not yet in the graph: run it now
+    const uint32_t* n_ptr = c->counters + (c->shard ? 6 : 0);
+    if (asse_status e = enqueue_bucket_sort(c, n_ptr, n_cand, s)) return e;
+    c->stats.kernel_launches += kBsKernels;
     CK(cudaMemcpyAsync(c->h_counters, c->counters, 64, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     prefetched = false;
-    // later slices sort on the device inside the end_slice graph (bound with 50 % headroom)
-    uint64_t B = kSortCap * 2ull;
-    while (B < (uint64_t)n_cand + n_cand / 2) B *= 2;
-    c->sort_bound = (uint32_t)std::min<uint64_t>(B, p.max_candidates);
+    // later slices sort on the device inside the end_slice graph (buckets sized for 1.5 n)
+    c->sort_bound = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(2ull * kRankCap, (uint64_t)n_cand + n_cand / 2),
+                                                 p.max_candidates);
     drop_graphs(c);
   }
   c->last_n = n_cand;

@@ -13,7 +13,6 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include <cub/block/block_radix_sort.cuh>
 
 #include "asse_tma.cuh"
 
@@ -750,141 +749,50 @@ __global__ void __launch_bounds__(512, 2) k_restore(RestoreParams p) {   // 2 CT
   pdl_trigger();
 }
 
-// In-graph device-wide sort for |CSIP| above the block sort (used once a slice needed it):
-// the radix sort runs over a host-chosen bound B >= |CSIP|, so no host round trip is
-// needed. Slots [n, B) get key 0xFFFFFFFF (a real ip of that value sorts first: the sort is
-// stable and real slots come first); counters[5] (set by k_sort when n > kSortCap) is
-// cleared when n <= B, else the host falls back to the exact-n path.
-__global__ void k_sort_prep(const uint32_t* __restrict__ n_ptr, uint32_t bound, uint32_t max_cand,
-                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* counters) {
-  const uint32_t n = min(*n_ptr, max_cand);
-  if (blockIdx.x == 0 && threadIdx.x == 0 && n <= bound) counters[5] = 0u;
-  for (uint32_t q = n + blockIdx.x * blockDim.x + threadIdx.x; q < bound; q += gridDim.x * blockDim.x) {
-    keys[q] = 0xFFFFFFFFu;
-    vals[q] = q;
-  }
-}
-// sorted order -> reports; slots >= n become empty reports (flags 0: not selected)
-__global__ void k_gather_bound(const ReportDev* __restrict__ in, const uint32_t* __restrict__ order,
-                               const uint32_t* __restrict__ n_ptr, uint32_t bound, uint32_t max_cand,
-                               ReportDev* __restrict__ out_all) {
-  const uint32_t n = min(*n_ptr, max_cand);
-  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < bound; q += gridDim.x * blockDim.x) {
-    if (q < n) out_all[q] = in[order[q]];
-    else out_all[q] = ReportDev{0xFFFFFFFFu, 0u, 0.0, 0u, 0u};
-  }
-}
-
-// gather reports in ascending-ip order (A24)
-__global__ void k_gather(const ReportDev* __restrict__ in, const uint32_t* __restrict__ order,
-                         uint32_t n, ReportDev* __restrict__ out_all) {
-  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
-    out_all[q] = in[order[q]];
-}
-
 // Sort of CSIP by ip (A24) and the est >= theta subset (A21), |CSIP| read on the device:
 //  * |CSIP| <= 2048: rank sort, one warp per element — CSIP ips are distinct (tuple <->
 //    LBS bijection, A16), so an element's position is the number of smaller ips and its
 //    position among the ABOVE_THETA reports counts the smaller flagged ips;
-//  * <= 8192: CTA 0 runs a block radix sort;
-//  * larger: counters[5] = 1 and the host runs the device-wide radix sort.
+//  * larger: counters[5] = 1 and the bucket sort below runs (k_bs_*; in the end_slice graph
+//    once a slice needed it, else from the host).
 // counters: [0] n_cand, [4] n_above, [5] big.
 constexpr int kSortThreads = 512;
 constexpr uint32_t kRankCap = 2048;
 constexpr int kSortBlocks = kRankCap / (kSortThreads / 32);   // 128: one warp per element
-constexpr uint32_t kSortCap = kSortThreads * 16;               // 8192
-
-template <int ITEMS>
-__device__ __forceinline__ void block_sort_emit(const ReportDev* __restrict__ rep, uint32_t n,
-                                                ReportDev* __restrict__ sorted, ReportDev* __restrict__ above,
-                                                uint32_t* counters, void* tmp_raw, uint32_t* warp_cnt) {
-  using BlockSort = cub::BlockRadixSort<uint32_t, kSortThreads, ITEMS, uint32_t, 4>;
-  auto& tmp = *reinterpret_cast<typename BlockSort::TempStorage*>(tmp_raw);
-  uint32_t keys[ITEMS], idx[ITEMS];
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const uint32_t q = threadIdx.x * ITEMS + j;       // blocked arrangement
-    keys[j] = (q < n) ? rep[q].ip : 0xFFFFFFFFu;
-    idx[j] = q;
-  }
-  BlockSort(tmp).Sort(keys, idx);                        // stable, ascending
-  uint32_t mine = 0, sel = 0;
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const uint32_t q = threadIdx.x * ITEMS + j;
-    if (q < n) {
-      const ReportDev r = rep[idx[j]];
-      sorted[q] = r;
-      if (r.flags & 2u) { sel |= 1u << j; mine++; }
-    }
-  }
-  // exclusive prefix over threads (thread order == ip order in the blocked layout)
-  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  uint32_t incl = mine;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, off);
-    if (lane >= (uint32_t)off) incl += t;
-  }
-  if (lane == 31) warp_cnt[wid] = incl;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0;
-    for (int w = 0; w < kSortThreads / 32; ++w) { const uint32_t t = warp_cnt[w]; warp_cnt[w] = acc; acc += t; }
-    counters[4] = acc;
-  }
-  __syncthreads();
-  uint32_t pos = warp_cnt[wid] + incl - mine;
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j)
-    if ((sel >> j) & 1u) above[pos++] = rep[idx[j]];
-}
 
 __global__ void __launch_bounds__(kSortThreads) k_sort(const ReportDev* __restrict__ rep, uint32_t* counters,
                                                        const uint32_t* n_ptr, uint32_t max_cand,
                                                        ReportDev* __restrict__ sorted,
                                                        ReportDev* __restrict__ above) {
-  using S16 = cub::BlockRadixSort<uint32_t, kSortThreads, 16, uint32_t, 4>;
-  union Smem {
-    typename S16::TempStorage radix;                   // the largest block-sort instance
-    struct { uint32_t key[kRankCap]; uint32_t above[kRankCap / 32]; } rank;
-  };
+  struct Smem { uint32_t key[kRankCap]; uint32_t above[kRankCap / 32]; };
   __shared__ __align__(16) Smem sm;
-  __shared__ uint32_t warp_cnt[kSortThreads / 32];
   pdl_wait();                                          // k_restore's reports and |CSIP|
   const uint32_t n = min(*n_ptr, max_cand);
   if (n == 0) return;
-  if (n > kSortCap) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) counters[5] = 1u;
-    return;
-  }
   if (n > kRankCap) {
-    if (blockIdx.x != 0) return;
-    if (n <= kSortThreads * 4) block_sort_emit<4>(rep, n, sorted, above, counters, &sm.radix, warp_cnt);
-    else if (n <= kSortThreads * 8) block_sort_emit<8>(rep, n, sorted, above, counters, &sm.radix, warp_cnt);
-    else block_sort_emit<16>(rep, n, sorted, above, counters, &sm.radix, warp_cnt);
+    if (blockIdx.x == 0 && threadIdx.x == 0) counters[5] = 1u;
     return;
   }
   // rank sort
   const uint32_t first = blockIdx.x * (kSortThreads / 32);
   if (first >= n) return;                              // CTA without elements
-  for (uint32_t j = threadIdx.x; j < kRankCap / 32; j += kSortThreads) sm.rank.above[j] = 0;
+  for (uint32_t j = threadIdx.x; j < kRankCap / 32; j += kSortThreads) sm.above[j] = 0;
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
     const ReportDev r = rep[j];
-    sm.rank.key[j] = r.ip;
-    if (r.flags & 2u) atomicOr(&sm.rank.above[j >> 5], 1u << (j & 31u));
+    sm.key[j] = r.ip;
+    if (r.flags & 2u) atomicOr(&sm.above[j >> 5], 1u << (j & 31u));
   }
   __syncthreads();
   const uint32_t q = first + (threadIdx.x >> 5);
   if (q >= n) return;
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t k = sm.rank.key[q];
+  const uint32_t k = sm.key[q];
   uint32_t r_all = 0, r_above = 0;
   for (uint32_t j = lane; j < n; j += 32) {
-    const uint32_t less = sm.rank.key[j] < k ? 1u : 0u;
+    const uint32_t less = sm.key[j] < k ? 1u : 0u;
     r_all += less;
-    r_above += less & (sm.rank.above[j >> 5] >> (j & 31u));
+    r_above += less & (sm.above[j >> 5] >> (j & 31u));
   }
   r_all = __reduce_add_sync(0xFFFFFFFFu, r_all);
   r_above = __reduce_add_sync(0xFFFFFFFFu, r_above);
@@ -895,6 +803,167 @@ __global__ void __launch_bounds__(kSortThreads) k_sort(const ReportDev* __restri
       above[r_above] = r;
       atomicAdd(counters + 4, 1u);
     }
+  }
+}
+
+// Bucket sort of CSIP by ip (A24) for |CSIP| > kRankCap, with the est >= theta subset in the
+// same order (A21). CSIP ips are distinct (A16), so placing every ip in the bucket of its top
+// bits and ranking it among its bucket (number of smaller ips) is an exact sort; the ranks
+// inside a bucket need no stability. B = 2^bits buckets (host-chosen, ~32 ips per bucket for
+// uniformly spread ips; any distribution is still sorted exactly, a crowded bucket only
+// costs time). |CSIP| is read on the device: every kernel does nothing when n <= kRankCap
+// (k_sort's rank sort handled it).
+struct BucketSortParams {
+  const ReportDev* rep;   // reports in slot order
+  const uint32_t* keys;   // ip per slot
+  const uint32_t* vals;   // report slot per slot
+  const uint32_t* n_ptr;
+  uint32_t max_cand, B, shift;   // shift = 32 - log2(B)
+  uint32_t* cnt;          // [B] ips per bucket (zeroed before k_bs_count)
+  uint32_t* off;          // [B] first position of each bucket
+  uint32_t* cur;          // [B] scatter cursors
+  uint32_t* acnt;         // [B] flagged reports per bucket
+  uint32_t* aoff;         // [B] first above-theta position of each bucket
+  uint32_t* tk;           // [max_cand] keys in bucket order
+  uint32_t* tv;           // [max_cand] slots in bucket order
+  uint32_t* arank;        // [max_cand] per sorted position: rank among the flagged, or ~0
+  uint32_t* pbkt;         // [max_cand] per sorted position: its bucket
+  ReportDev* sorted;
+  ReportDev* above;
+  uint32_t* counters;
+};
+
+__device__ __forceinline__ uint32_t bs_n(const BucketSortParams& p) { return min(*p.n_ptr, p.max_cand); }
+
+__global__ void __launch_bounds__(256) k_bs_count(BucketSortParams p) {
+  const uint32_t n = bs_n(p);
+  if (n <= kRankCap) return;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
+    atomicAdd(p.cnt + (p.keys[q] >> p.shift), 1u);
+}
+
+// exclusive scan of in[0..B) into out (and out2 if given) by one CTA of 1024 threads
+__device__ __forceinline__ uint32_t bs_block_scan(const uint32_t* in, uint32_t* out, uint32_t* out2, uint32_t B) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t carry;
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < B; base += blockDim.x) {
+    const uint32_t q = base + threadIdx.x;
+    const uint32_t v = q < B ? in[q] : 0u;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= (uint32_t)o) incl += t;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t w = (lane < blockDim.x / 32) ? wsum[lane] : 0u;
+      uint32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+        if (lane >= (uint32_t)o) wi += t;
+      }
+      wsum[lane] = wi - w;                              // exclusive prefix of the warp sums
+    }
+    __syncthreads();
+    const uint32_t ex = carry + wsum[wid] + incl - v;
+    if (q < B) {
+      out[q] = ex;
+      if (out2) out2[q] = ex;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = ex + v;
+    __syncthreads();
+  }
+  return carry;
+}
+
+__global__ void __launch_bounds__(1024) k_bs_scan(BucketSortParams p) {
+  if (bs_n(p) <= kRankCap) return;
+  bs_block_scan(p.cnt, p.off, p.cur, p.B);
+}
+
+__global__ void __launch_bounds__(256) k_bs_scatter(BucketSortParams p) {
+  const uint32_t n = bs_n(p);
+  if (n <= kRankCap) return;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const uint32_t k = p.keys[q];
+    const uint32_t pos = atomicAdd(p.cur + (k >> p.shift), 1u);
+    p.tk[pos] = k;
+    p.tv[pos] = p.vals[q];
+  }
+}
+
+// one warp per bucket: rank every ip among its bucket (all ips and the flagged ones)
+constexpr uint32_t kBsWarps = 8, kBsCap = 512;   // keys staged per warp in shared memory
+constexpr uint32_t kBsMaxLgB = 16, kBsMaxB = 1u << kBsMaxLgB;   // buckets at most
+constexpr int kBsKernels = 6;
+__global__ void __launch_bounds__(32 * kBsWarps) k_bs_bucket(BucketSortParams p) {
+  __shared__ uint32_t skey[kBsWarps][kBsCap];
+  __shared__ uint32_t sflag[kBsWarps][kBsCap / 32];
+  const uint32_t n = bs_n(p);
+  if (n <= kRankCap) return;
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  const uint32_t b = blockIdx.x * kBsWarps + w;
+  if (b >= p.B) return;
+  const uint32_t s = p.cnt[b], o = p.off[b];
+  const bool staged = s <= kBsCap;
+  uint32_t nflag = 0;
+  if (staged) {
+    for (uint32_t j = lane; j < kBsCap / 32; j += 32) sflag[w][j] = 0;
+    __syncwarp();
+    for (uint32_t j = lane; j < s; j += 32) {
+      skey[w][j] = p.tk[o + j];
+      if (p.rep[p.tv[o + j]].flags & 2u) atomicOr(&sflag[w][j >> 5], 1u << (j & 31u));
+    }
+    __syncwarp();
+  }
+  for (uint32_t j0 = 0; j0 < s; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    uint32_t kj = 0, r = 0, ra = 0;
+    bool fj = false;
+    if (j < s) {
+      kj = staged ? skey[w][j] : p.tk[o + j];
+      const ReportDev rj = p.rep[p.tv[o + j]];
+      fj = (rj.flags & 2u) != 0;
+      for (uint32_t i = 0; i < s; ++i) {
+        const uint32_t ki = staged ? skey[w][i] : p.tk[o + i];
+        const uint32_t less = ki < kj ? 1u : 0u;
+        r += less;
+        const uint32_t fi = staged ? (sflag[w][i >> 5] >> (i & 31u)) & 1u
+                                   : ((p.rep[p.tv[o + i]].flags >> 1) & 1u);
+        ra += less & fi;
+      }
+      const uint32_t pos = o + r;
+      p.sorted[pos] = rj;
+      p.arank[pos] = fj ? ra : 0xFFFFFFFFu;
+      p.pbkt[pos] = b;
+    }
+    nflag += __popc(__ballot_sync(0xFFFFFFFFu, fj));
+  }
+  if (lane == 0) p.acnt[b] = nflag;
+}
+
+__global__ void __launch_bounds__(1024) k_bs_scan2(BucketSortParams p) {
+  if (bs_n(p) <= kRankCap) return;
+  const uint32_t tot = bs_block_scan(p.acnt, p.aoff, nullptr, p.B);
+  if (threadIdx.x == 0) {
+    p.counters[4] = tot;
+    p.counters[5] = 0u;                                 // handled on the device
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bs_above(BucketSortParams p) {
+  const uint32_t n = bs_n(p);
+  if (n <= kRankCap) return;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const uint32_t ar = p.arank[q];
+    if (ar != 0xFFFFFFFFu) p.above[p.aoff[p.pbkt[q]] + ar] = p.sorted[q];
   }
 }
 
