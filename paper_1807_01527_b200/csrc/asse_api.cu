@@ -1209,6 +1209,11 @@ static asse_status collect_finish(Ctx* c, uint32_t mode, uint32_t K, asse_report
                                                  p.max_candidates);
     drop_graphs(c);
   }
+  if (c->sort_bound > kRankCap && n_cand > c->sort_bound) {
+    // |CSIP| outgrew the bucket sort's sizing (~32 ips per bucket): resize for later slices
+    c->sort_bound = (uint32_t)std::min<uint64_t>((uint64_t)n_cand + n_cand / 2, p.max_candidates);
+    drop_graphs(c);
+  }
   c->last_n = n_cand;
   c->last_above = n_cand ? c->h_counters[4] : 0;
   c->have_reports = true;
