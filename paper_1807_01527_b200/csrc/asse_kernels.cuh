@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(fold_threads<CB, WEIGH>(), CB == 1 ? ASSE_FOLD
       }
       const uint32_t field = WEIGH ? 0u : (stouch[cc * 16u] >> tshift) & 0xFFFFu;
       uint32_t v[LW];
-      uint32_t cnt = 0, accbits = 0;
+      uint32_t accbits = 0;
       bool changed = false;
 #pragma unroll
       for (int q = 0; q < NW; ++q) {
@@ -470,7 +470,6 @@ __global__ void __launch_bounds__(fold_threads<CB, WEIGH>(), CB == 1 ? ASSE_FOLD
         // checkAT (Alg. 1): two intervals of the cyclic window
         const uint32_t vx = x | G;
         const uint32_t act = (in_range(vx, x, LO1[q], HI1[q]) | in_range(vx, x, LO2[q], HI2[q])) & G;
-        cnt += __popc(act);
         accbits |= act >> ((CB == 1 ? 7 : 15) - q);
         // preserveAT for slice t+1 (Alg. 2), only in words holding swept blocks
         if (!WEIGH && (swept_mask & (1u << q))) {
@@ -517,6 +516,7 @@ __global__ void __launch_bounds__(fold_threads<CB, WEIGH>(), CB == 1 ? ASSE_FOLD
       }
       // |ATV|^{k'} of every ATV in the chunk with one warp reduction: each ATV's
       // lanes add into their own FIELD-bit slot (max 16*LPA fits the slot)
+      const uint32_t cnt = __popc(accbits);   // the guard bits of every word, gathered into 16 distinct bits
       const uint32_t packed = __reduce_add_sync(0xFFFFFFFFu, cnt << fshift);
       const uint32_t w = (FIELD == 32) ? packed : ((packed >> fshift) & ((1u << FIELD) - 1u));
       uint32_t tot;
