@@ -1084,6 +1084,7 @@ struct BarrierParams {
 // Cross-rank barrier over signal pads: publish `epoch` into slot [rank] of every peer's
 // pad (release, system scope), then wait until every slot of our pad reached `epoch`
 // (acquire). Called by one whole block of >= world threads.
+constexpr uint64_t kBarrierTimeoutNs = 30ull * 1000000000ull;   // 30 s
 __device__ __forceinline__ void barrier_ranks(uint32_t* const* pads, uint32_t world, uint32_t rank,
                                               uint32_t epoch) {
   const uint32_t w = threadIdx.x;
@@ -1095,8 +1096,18 @@ __device__ __forceinline__ void barrier_ranks(uint32_t* const* pads, uint32_t wo
   if (w < world) {
     const uint32_t* src = pads[rank] + w;
     uint32_t v;
+    uint64_t t0 = 0;
+    uint32_t spins = 0;
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(src) : "memory");
+      // watchdog: a rank that never arrives (a crashed peer, a protocol fault) ends the
+      // kernel with an error after kBarrierTimeoutNs instead of hanging the GPU
+      if ((++spins & 1023u) == 0) {
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > kBarrierTimeoutNs) __trap();
+      }
     } while ((int32_t)(v - epoch) < 0);
   }
   __syncthreads();
