@@ -84,3 +84,13 @@ def _run_virtual_ranks(name, D, N, T, shard, variant):
             if d and not shard:
                 assert (ranks[d].pool() == pool0).all()
     del bufs
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("D,shard", [(8, 1), (2, 0)])
+def test_virtual_ranks_full_size_c5(cuda_device, D, shard):
+    """BASELINE.json configs[4] at full size: the 100M-packet C5 slice split round-robin
+    over D ranks (12.5M / 50M packets each, the packet-owned scan on every rank), merged
+    and closed; every rank equals the oracle fed the whole slice ("results must be
+    identical for every D")."""
+    _run_virtual_ranks("C5", D, None, 2, shard, 0)
