@@ -487,23 +487,19 @@ __global__ void __launch_bounds__(kBinThreads, 1) k_scan_bin(const uint2* __rest
     if (bp.prof && gtid == 0) { bp.prof[me * 16 + 9 + 2 * grp] = cwait; bp.prof[me * 16 + 10 + 2 * grp] = cwork; }
   }
   // every round consumed by this CTA: every producer has published every round, so all
-  // overflow REDs are performed; OR the owned words into the global bitmap
+  // overflow REDs are performed; OR the owned words into the global bitmap with one bulk
+  // reduction (TMA cp.reduce.async.bulk .or: the owned words are contiguous in global
+  // memory), performed in L2 — no read of the global words by the SM
+  fence_proxy_async_smem();                     // this thread's shared atomics -> async proxy
   named_bar(4, kComputeThreads);
   const uint64_t w0 = (uint64_t)me * bp.wpo;
-  if (w0 < bp.total_words) {
-    const uint32_t nw = (uint32_t)umin64(bp.wpo, bp.total_words - w0);
-    uint4* gdst = reinterpret_cast<uint4*>(bp.sp.touch + bp.base_word + w0);
-    const uint4* ssrc = reinterpret_cast<const uint4*>(sbm);
-    for (uint32_t q = threadIdx.x; q < (nw >> 2); q += kComputeThreads) {
-      const uint4 s = ssrc[q];
-      if (s.x | s.y | s.z | s.w) {
-        uint4 gv;
-        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(gv.x), "=r"(gv.y), "=r"(gv.z), "=r"(gv.w) : "l"(gdst + q));
-        gv.x |= s.x; gv.y |= s.y; gv.z |= s.z; gv.w |= s.w;
-        gdst[q] = gv;
-      }
-    }
+  if (threadIdx.x == 0 && w0 < bp.total_words) {
+    const uint32_t nw = (uint32_t)umin64(bp.wpo, bp.total_words - w0);   // multiple of 4 (16 B)
+    uint32_t* gdst = bp.sp.touch + bp.base_word + w0;
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.or.b32 [%0], [%1], %2;"
+                 :: "l"(gdst), "r"(smem_u32(sbm)), "r"(nw * 4u) : "memory");
+    bulk_commit();
+    bulk_wait0();                                // complete before the CTA's shared memory goes away
   }
 }
 
