@@ -63,7 +63,8 @@ struct Ctx {
   uint32_t own_O = 0, own_lg_ngrp = 0, own_lg_wg = 0, own_tile = 0;
   size_t own_smem = 0;
   uint2* own_queue = nullptr;         // [NB][O][QG][QCAP]
-  uint32_t* own_sync = nullptr;
+  uint32_t* own_sync = nullptr;      // two sets of the packet-owned scan's counters (launch parity)
+  uint32_t own_parity = 0;
   cudaStream_t stream = nullptr, copy_stream = nullptr;
   cudaStream_t d2h_stream = nullptr;  // result copies of end_slice (off the context stream)
   cudaEvent_t ev_done = nullptr;      // end of a slice's kernels on the context stream
@@ -393,7 +394,8 @@ static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const Sc
   const size_t sync_words = (2 * kOwnNB + (size_t)kOwnNB * O * kOwnQG) * kBinPad;
   if (!c->own_queue) {
     CK(cudaMalloc(&c->own_queue, (size_t)kOwnNB * O * kOwnQG * kOwnQCap * sizeof(uint2)));
-    CK(cudaMalloc(&c->own_sync, sync_words * 4));
+    CK(cudaMalloc(&c->own_sync, 2 * sync_words * 4));
+    CK(cudaMemsetAsync(c->own_sync, 0, 2 * sync_words * 4, st));
   }
   const int dev = c->device & 63;
   if (!g_bin_last[dev]) CK(cudaEventCreateWithFlags(&g_bin_last[dev], cudaEventDisableTiming));
@@ -401,8 +403,13 @@ static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const Sc
   OwnScanParams op{};
   op.sp = sp;
   op.queue = c->own_queue;
-  op.qcnt = c->own_sync + 2 * kOwnNB * kBinPad;
-  op.sync = c->own_sync;
+  // this launch's counters are zero (set at allocation or by the previous launch); the
+  // kernel zeroes the other set for the next launch (scans of a device are serialised)
+  uint32_t* cur = c->own_sync + (size_t)c->own_parity * sync_words;
+  op.qcnt = cur + 2 * kOwnNB * kBinPad;
+  op.sync = cur;
+  op.sync_next = c->own_sync + (size_t)(c->own_parity ^ 1u) * sync_words;
+  op.sync_words = (uint32_t)sync_words;
   op.O = O;
   op.lg_ngrp = c->own_lg_ngrp;
   op.lg_wg = c->own_lg_wg;
@@ -413,7 +420,6 @@ static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const Sc
     if (!dprof) CK(cudaMalloc(&dprof, 16 * 1024 * 8));
     op.prof = dprof;
   }
-  CK(cudaMemsetAsync(c->own_sync, 0, sync_words * 4, st));
   cudaError_t e;
   const asse_config& g = c->cfg;
   const bool c3 = g.u == 4 && g.c == 12 && g.s == 6 && g.g == 512 && g.r == 4 && c->own_lg_ngrp == 3 && c->own_lg_wg == 1 &&
@@ -430,6 +436,7 @@ static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const Sc
     return ASSE_E_CAPACITY;
   }
   CK(e);
+  c->own_parity ^= 1u;                           // launched: the next call uses the set it zeroes
   CK(cudaEventRecord(g_bin_last[dev], st));
   if (op.prof) {
     std::vector<unsigned long long> h((size_t)G * 16);

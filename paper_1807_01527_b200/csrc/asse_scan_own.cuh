@@ -107,7 +107,9 @@ struct OwnScanParams {
   ScanParams sp;          // hashing parameters and the global touch bitmap
   uint2* queue;           // [NB][O][QG][QCAP] rings of entries (see own_bin_two)
   uint32_t* qcnt;         // [NB][O][QG] x kBinPad: entries ever reserved (monotone per launch)
-  uint32_t* sync;         // [2 NB] x kBinPad: rounds published per buffer, then owners done; zeroed
+  uint32_t* sync;         // [2 NB] x kBinPad: rounds published per buffer, then owners done; zero at launch
+  uint32_t* sync_next;    // the other counter set (sync + qcnt of the next launch): zeroed here
+  uint32_t sync_words;
   uint32_t O;             // owners = F << lg_ngrp (<= gridDim.x)
   uint32_t lg_ngrp;       // word groups per ATV (log2)
   uint32_t lg_wg;         // words per group (log2)
@@ -263,6 +265,9 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   const uint8_t* body = reinterpret_cast<const uint8_t*>(pk + head);
 
   if (warp == kOwnSigWarp) {                     // ---------------- round publication
+    // first, this CTA's share of the next launch's counters (no memset launch per call)
+    for (uint32_t q = (me * 32u + lane) * 4u; q < op.sync_words; q += G * 32u * 4u)
+      *reinterpret_cast<uint4*>(op.sync_next + q) = make_uint4(0u, 0u, 0u, 0u);
     if (lane == 0)
       for (uint32_t tf = 0; tf < R; ++tf) {
         mbar_wait_suspend(&sigbar[tf % kSig], (tf / kSig) & 1u);   // every binning warp wrote round tf

@@ -1,4 +1,4 @@
-"""Fixed vs per-round cost of k_scan_bin: time scans of R rounds (R * 148 * 2048 packets of
+"""Fixed vs per-round cost of k_scan_bin (argv[1] = 2) or k_scan_own (3): time scans of R rounds (R * 148 * 2048 packets of
 the C5 mixture) for several R and fit t = a + b R."""
 import sys
 sys.path.insert(0, ".")
@@ -9,7 +9,7 @@ from paper_1807_01527_b200 import asse
 
 p = dict(PRESETS["C5"])
 ctx = asse.Asse(**p)
-ctx.set_scan_variant(2)
+ctx.set_scan_variant(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
 G = torch.cuda.get_device_properties(0).multi_processor_count
 g = Generator("C5")
 buf = torch.empty(2 * 100_000_000, dtype=torch.int32, device="cuda")
@@ -17,7 +17,7 @@ g.slice_cuda(0, buf.data_ptr())
 torch.cuda.synchronize()
 st = torch.cuda.ExternalStream(ctx.stream())
 res = []
-for R in (1, 2, 4, 8, 16, 32, 64, 128, 256, 329):
+for R in (8, 12, 16, 24, 32, 48, 64, 128, 256, 329):
     n = min(100_000_000, R * G * 2048)
     ts = []
     for rep in range(6):
