@@ -442,8 +442,19 @@ static asse_status launch_scan_own(Ctx* c, const uint2* pk, uint64_t n, const Sc
     std::vector<unsigned long long> h((size_t)G * 16);
     CK(cudaStreamSynchronize(st));
     CK(cudaMemcpy(h.data(), op.prof, h.size() * 8, cudaMemcpyDeviceToHost));
-    const char* nm[13] = {"b_bin", "b_wait_reserve", "b_copy", "b_bin_wait_tile", "-", "-",
-                          "-", "-", "-", "c0_wait", "c0_drain", "c1_wait", "c1_drain"};
+    const char* nm[13] = {"b_bin", "b_wait_reserve", "b_copy", "b_bin_wait_tile", "t_start", "t_shipped",
+                          "t_drained", "-", "-", "c0_wait", "c0_drain", "c1_wait", "c1_drain"};
+    {   // timeline (globaltimer ns) relative to the earliest CTA start
+      unsigned long long t0 = ~0ull;
+      for (uint32_t b = 0; b < G; ++b) t0 = std::min(t0, h[b * 16 + 4]);
+      for (int q = 4; q <= 6; ++q) {
+        unsigned long long mn = ~0ull, mx = 0;
+        for (uint32_t b = 0; b < G; ++b) {
+          if (q == 6 || b < G) { mn = std::min(mn, h[b * 16 + q] - t0); mx = std::max(mx, h[b * 16 + q] - t0); }
+        }
+        fprintf(stderr, "k_scan_own timeline %s: min %.1f us max %.1f us\n", nm[q], mn / 1e3, mx / 1e3);
+      }
+    }
     fprintf(stderr, "k_scan_own n=%llu G=%u O=%u:", (unsigned long long)n, G, O);
     for (int q = 0; q < 13; ++q) {
       double sum = 0, mx = 0;

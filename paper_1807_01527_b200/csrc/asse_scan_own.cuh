@@ -137,6 +137,12 @@ __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t phase)
   }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void sts64_if(bool pred, uint32_t addr, uint32_t a, uint32_t b) {
   asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.shared.v2.u32 [%1], {%2, %3};\n}"
                :: "r"((uint32_t)pred), "r"(addr), "r"(a), "r"(b) : "memory");
@@ -262,6 +268,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
     mbar_fence_init();
   }
   __syncthreads();
+  if (op.prof && threadIdx.x == 0) op.prof[me * 16 + 4] = gtimer();   // tools: timeline (ns)
   const uint8_t* body = reinterpret_cast<const uint8_t*>(pk + head);
 
   if (warp == kOwnSigWarp) {                     // ---------------- round publication
@@ -397,8 +404,10 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
       named_bar(1, kBinT);                       // bins of round t final; staging sf and counts reusable
       c1 = clock64(); pc[2] += c1 - c0; c0 = c1;
     }
-    if (op.prof && tid == 0)
+    if (op.prof && tid == 0) {
       for (int q = 0; q < 4; ++q) op.prof[me * 16 + q] = pc[q];
+      op.prof[me * 16 + 5] = gtimer();          // last round shipped
+    }
   } else if (owner) {                            // ---------------- queue-draining warps
     const uint32_t cid = warp - kOwnConsWarp0;
     const uint32_t grp = cid / (kOwnConsWarps / kOwnNGR);
@@ -465,6 +474,7 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   // bitmap: slice word ((y << c | x) << lg_wg) | sub -> global ATV ((y F + z) << c) + x,
   // word grp * WG + sub
   named_bar(8, kComputeThreads);
+  if (op.prof && threadIdx.x == 0) op.prof[me * 16 + 6] = gtimer();   // every round drained
   if (!owner) return;
   __threadfence();
   const ScanParams& p = op.sp;
@@ -474,8 +484,9 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   const uint32_t row_words = (p.fmask + 1u) << p.c;          // ATVs per row
   // fire-and-forget ORs (RED): no read of the global word, so nothing waits on L2 round
   // trips (the read-OR-write it replaces cost ~14 us per call: C5 scan 0.722 -> 0.707 ms,
-  // C3 0.181 -> 0.166 ms; gpurun_out/sweep_wb.jsonl); atomic, so overflow REDs of other
-  // CTAs and earlier calls of the slice need no ordering argument
+  // C3 0.181 -> 0.166 ms; profiles/r02_sweeps/sweep_wb.jsonl; plain 8-B stores measured 3 us
+  // slower than the REDs); atomic, so overflow REDs of other CTAs and earlier calls of the
+  // slice need no ordering argument
   if (op.lg_wg >= 1) {                            // 8-B chunks
     const uint32_t n2 = slice_words >> 1;
     for (uint32_t q = threadIdx.x; q < n2; q += kComputeThreads) {
