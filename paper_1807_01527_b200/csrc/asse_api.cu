@@ -84,6 +84,8 @@ struct Ctx {
   RestoreParams rp0{};              // geometry part of the restore parameters
   uint32_t* d_clock = nullptr;      // device copy of C0, refreshed from h_clock per slice
   uint32_t* h_clock = nullptr;      // pinned
+  uint32_t d_clock_known = ~0u;     // the value d_clock holds once the queued work ran (~0: unknown)
+  bool sort_advances_clock = false; // set while the end_slice sequence is enqueued
   cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [timing][mode]
   size_t restore_smem = 0;
   uint32_t* ws = nullptr;
@@ -1082,7 +1084,8 @@ static asse_status enqueue_bucket_sort(Ctx* c, const uint32_t* n_ptr, uint64_t b
 static asse_status enqueue_sort(Ctx* c) {
   const uint32_t* n_ptr = c->counters + (c->shard ? 6 : 0);
   CK(launch_pdl(k_sort, dim3(kSortBlocks), dim3(kSortThreads), 0, c->stream, (const ReportDev*)c->rep,
-                c->counters, n_ptr, (uint32_t)c->cfg.max_candidates, c->rep_sorted, c->rep_above));
+                c->counters, n_ptr, (uint32_t)c->cfg.max_candidates, c->rep_sorted, c->rep_above,
+                c->sort_advances_clock ? c->d_clock : nullptr, c->two_k));
   // |CSIP| beyond the rank sort was seen: the bucket sort runs in the graph from then on
   // (its kernels return at once while |CSIP| <= kRankCap)
   if (c->sort_bound > kRankCap) return enqueue_bucket_sort(c, n_ptr, c->sort_bound, c->stream);
@@ -1290,6 +1293,7 @@ asse_status asse_end_slice_begin(void* ctx) {
   if (c->collect_pending) CK(cudaStreamWaitEvent(s, c->ev_collect, 0));
   *c->h_clock = c->C0;
   CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
+  c->d_clock_known = c->C0;
   CK(cudaMemsetAsync(c->xchg, 0, 64, s));
   CK(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, s));
   const FoldParams fp = fold_params(c, c->merged, c->kp);
@@ -1326,11 +1330,16 @@ static asse_status end_slice_enqueue(Ctx* c, uint32_t mode, uint32_t* K_out) {
   if (c->collect_pending) CK(cudaStreamWaitEvent(s, c->ev_collect, 0));
   // the per-slice ACT base reaches the kernels through device memory, so the captured
   // graph is identical for every slice (host copies stay outside the graph)
-  *c->h_clock = c->C0;
-  CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
+  if (c->d_clock_known != c->C0) {           // else the previous slice's k_sort advanced it
+    *c->h_clock = c->C0;
+    CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
+  }
+  c->d_clock_known = ~0u;
+  c->sort_advances_clock = true;
   if ((c->peers && c->sync_mode != 1) || c->shard) {
     asse_status st = enqueue_end_slice(c, mode, timing, false);   // epochs / phases change per slice
     c->begun = false;
+    c->sort_advances_clock = false;
     if (st != ASSE_OK) return st;
   } else {
     cudaGraphExec_t& ge = c->graph[timing ? 1 : 0][mode];
@@ -1338,6 +1347,7 @@ static asse_status end_slice_enqueue(Ctx* c, uint32_t mode, uint32_t* K_out) {
       cudaGraph_t g = nullptr;
       CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       asse_status st = enqueue_end_slice(c, mode, timing, true);
+      c->sort_advances_clock = false;
       cudaError_t ce = cudaStreamEndCapture(s, &g);
       if (st != ASSE_OK) { if (g) cudaGraphDestroy(g); return st; }
       CK(ce);
@@ -1346,6 +1356,8 @@ static asse_status end_slice_enqueue(Ctx* c, uint32_t mode, uint32_t* K_out) {
     }
     CK(cudaGraphLaunch(ge, s));
   }
+  c->sort_advances_clock = false;
+  c->d_clock_known = (c->C0 + 1u) % c->two_k;   // collect_enqueue advances C0 to the same value
   *K_out = K;
   return collect_enqueue(c, mode, K, true);
 }
@@ -1409,6 +1421,7 @@ asse_status asse_query_window(void* ctx, uint32_t k_prime, asse_report* h_out, u
   if (c->collect_pending) CK(cudaStreamWaitEvent(s, c->ev_collect, 0));
   *c->h_clock = (c->C0 + c->two_k - 1) % c->two_k;          // ACT base of the last closed slice
   CK(cudaMemcpyAsync(c->d_clock, c->h_clock, 4, cudaMemcpyHostToDevice, s));
+  c->d_clock_known = *c->h_clock;                            // the next end_slice re-uploads C0
   CK(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, s));
   const FoldParams fp = fold_params(c, nullptr, k_prime);
   if (c->cb == 1) launch_fold<1, true>(c->lpa_log2, c->q_log2, fold_blocks(c), s, fp);

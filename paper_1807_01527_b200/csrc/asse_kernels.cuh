@@ -763,10 +763,14 @@ constexpr int kSortBlocks = kRankCap / (kSortThreads / 32);   // 128: one warp p
 __global__ void __launch_bounds__(kSortThreads) k_sort(const ReportDev* __restrict__ rep, uint32_t* counters,
                                                        const uint32_t* n_ptr, uint32_t max_cand,
                                                        ReportDev* __restrict__ sorted,
-                                                       ReportDev* __restrict__ above) {
+                                                       ReportDev* __restrict__ above,
+                                                       uint32_t* clock, uint32_t two_k) {
   struct Smem { uint32_t key[kRankCap]; uint32_t above[kRankCap / 32]; };
   __shared__ __align__(16) Smem sm;
   pdl_wait();                                          // k_restore's reports and |CSIP|
+  // a9: the next slice's ACT base, advanced on the device (k_fold and k_restore of this
+  // slice are complete), so no host-to-device copy precedes the next end_slice
+  if (clock && blockIdx.x == 0 && threadIdx.x == 0) *clock = (*clock + 1u == two_k) ? 0u : *clock + 1u;
   const uint32_t n = min(*n_ptr, max_cand);
   if (n == 0) return;
   if (n > kRankCap) {
