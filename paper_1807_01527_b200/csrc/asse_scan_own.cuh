@@ -268,6 +268,9 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
     mbar_fence_init();
   }
   __syncthreads();
+#ifdef ASSE_OWN_EMPTY
+  return;                                        // tools only: launch + prologue cost (no scan)
+#endif
   if (op.prof && threadIdx.x == 0) op.prof[me * 16 + 4] = gtimer();   // tools: timeline (ns)
   const uint8_t* body = reinterpret_cast<const uint8_t*>(pk + head);
 
@@ -476,6 +479,9 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   named_bar(8, kComputeThreads);
   if (op.prof && threadIdx.x == 0) op.prof[me * 16 + 6] = gtimer();   // every round drained
   if (!owner) return;
+#ifdef ASSE_OWN_NO_WB
+  return;                                        // tools only: timing without the write-back (wrong results)
+#endif
   __threadfence();
   const ScanParams& p = op.sp;
   const uint32_t z = me >> op.lg_ngrp, grp = me & ((1u << op.lg_ngrp) - 1u);
