@@ -813,6 +813,16 @@ asse_status asse_init(const asse_config* cfg, void** out) {
       for (uint32_t j = 0; j < p.c; ++j) known[(c->shift[y] + j) % c->W] = 1;
       rp.ov[y] = ov;
       rp.nfree[y] = nf;
+      {   // free positions (ascending) as at most two contiguous runs
+        uint32_t n1 = 0;
+        while (n1 < nf && rp.freepos[y][n1] == rp.freepos[y][0] + n1) ++n1;
+        uint32_t n2 = 0;
+        while (n1 + n2 < nf && rp.freepos[y][n1 + n2] == rp.freepos[y][n1] + n2) ++n2;
+        rp.dep_ok[y] = (n1 + n2 == nf) ? 1 : 0;
+        rp.dep_n1[y] = (uint8_t)n1;
+        rp.dep_sh1[y] = nf ? rp.freepos[y][0] : 0;
+        rp.dep_sh2[y] = (n1 < nf) ? (uint8_t)(rp.freepos[y][n1] - n1) : 0;
+      }
       rp.use_enum_max[y] = (nf <= 20) ? 4u : 0u;
     }
     c->restore_smem = (size_t)p.r * ((c->E + 31) / 32) * 4;
@@ -1584,6 +1594,12 @@ asse_status asse_set_host_barrier(void* ctx, asse_host_barrier_fn fn, void* arg)
 }
 
 // ------------------------------------------------------------ CUDA IPC helpers
+#ifdef ASSE_RESTORE_PROF
+// tools only (ASSE_RESTORE_PROF build): copy the per-CTA restore timeline marks
+extern "C" int asse_debug_restore_prof(unsigned long long* out, unsigned n) {
+  return (int)cudaMemcpyFromSymbol(out, g_restore_prof, (size_t)n * 8 * 8);
+}
+#endif
 static_assert(sizeof(cudaIpcMemHandle_t) == ASSE_IPC_HANDLE_BYTES, "IPC handle size");
 
 asse_status asse_ipc_alloc(int32_t device, uint64_t bytes, void** d_ptr, uint8_t* handle) {

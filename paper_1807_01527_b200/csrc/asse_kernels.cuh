@@ -585,6 +585,10 @@ struct RestoreParams {
   uint32_t nfree[kMaxR];    // c - popc(ov[y])
   uint32_t use_enum_max[kMaxR];  // enumerate the 2^nfree completions when 2^nfree <= this * |SA|
   uint8_t freepos[kMaxR][32];    // free bit positions of x_y
+  // the free positions as at most two ascending runs: completion bits [0, n1) shift up by
+  // sh1 (= freepos[0]), bits [n1, nf) by sh2 (= freepos[n1] - n1); dep_ok = 0: more runs,
+  // the freepos loop is used
+  uint8_t dep_n1[kMaxR], dep_sh1[kMaxR], dep_sh2[kMaxR], dep_ok[kMaxR];
   // Alg. 5 / Eq. 5 for every restored candidate (fused)
   const uint32_t* active;        // active bits, wpa words per ATV
   const unsigned long long* aat; // AAT[y][z]
@@ -618,11 +622,26 @@ __device__ __forceinline__ uint32_t place_row(uint32_t x, uint32_t sh, uint32_t 
 // x_y and tests SA membership — whichever is fewer probes.
 constexpr uint32_t kPartSmem = 2048;   // partial LBS kept in shared memory per level buffer
 
+#ifdef ASSE_RESTORE_PROF
+__device__ unsigned long long g_restore_prof[4096][8];   // tools only: per-CTA globaltimer marks
+#define RPROF(k) do { if (threadIdx.x == 0 && blockIdx.x < 4096) { unsigned long long t_; \
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_restore_prof[blockIdx.x][k] = t_; } } while (0)
+#else
+#define RPROF(k) ((void)0)
+#endif
+// Latency (per-CTA globaltimer marks, tools/restore_timeline.py, C3): prologue 1.8 us, rows
+// 0-2 ~1.3 us each, the last row with Alg. 5 5.1 us, when each row took three CTA barriers,
+// a dependent constant-bank load per free bit of the enumeration and row 0's list load
+// after the prologue, and the last row waited for its global slot before loading the NAT
+// words. Now: one barrier per row (three rotating counters), the free bits deposited as at
+// most two contiguous runs (host-derived; a loop otherwise), row 0's first 32 options of the
+// part prefetched in the prologue, the NAT loads issued while the slot atomic is in flight.
 __global__ void __launch_bounds__(512, 2) k_restore(RestoreParams p) {   // 2 CTAs per SM: one wave of F x parts
   extern __shared__ uint32_t s_bits[];  // r * E/32 words of SA(y, z) membership
   __shared__ uint32_t s_part[2][kPartSmem];
   __shared__ uint32_t s_nsa[kMaxR];
-  __shared__ uint32_t s_next, s_nin;
+  __shared__ uint32_t s_cnt[3];         // output count of row y: s_cnt[y % 3]
+  __shared__ uint32_t s_pre[32];        // row 0 (list scan): options part + j * parts, j < 32
   __shared__ double s_up;
   const uint32_t z = blockIdx.x / p.parts;
   const uint32_t part = blockIdx.x % p.parts;
@@ -632,31 +651,42 @@ __global__ void __launch_bounds__(512, 2) k_restore(RestoreParams p) {   // 2 CT
   // partial buffers: slots < kPartSmem in shared memory, the rest in the global workspace
   uint32_t* gbuf[2] = {p.ws + (size_t)blockIdx.x * 2 * p.ws_cap,
                        p.ws + (size_t)blockIdx.x * 2 * p.ws_cap + p.ws_cap};
+  RPROF(0);
   pdl_wait();                                         // k_fold's SA lists, bits, AAT, active bits
-  if (threadIdx.x < p.r) s_nsa[threadIdx.x] = p.sa_cnt[threadIdx.x * p.F + z];
-  if (threadIdx.x == 0) {
+  RPROF(1);
+  // prologue, one round trip: |SA(y, z)|, row 0's prefetched options, UP, the SA bits
+  if (threadIdx.x < p.r) s_nsa[threadIdx.x] = __ldcg(p.sa_cnt + threadIdx.x * p.F + z);
+  if (threadIdx.x >= 32 && threadIdx.x < 64) {
+    const uint32_t j = threadIdx.x - 32, o = part + j * p.parts;
+    s_pre[j] = (o < E) ? __ldcg(p.sa_list + (size_t)z * E + o) : 0u;
+  }
+  if (threadIdx.x == 64) {
     // UP_{k'}^{z} = prod_y AAT[y][z] / (g 2^c) (Eq. 4), same product order as the oracle
     double up = 0.0;
     for (uint32_t y = 0; y < p.r; ++y) {
-      const double P = (double)p.aat[y * p.F + z] / p.cells;
+      const double P = (double)__ldcg(p.aat + y * p.F + z) / p.cells;
       up = (y == 0) ? P : up * P;
     }
     s_up = up;
-    s_nin = 1;
-    s_part[0][0] = 0;
+  }
+  if (threadIdx.x == 96) {
+    s_cnt[0] = 0; s_cnt[1] = 0; s_cnt[2] = 0;
+    s_part[0][0] = 0;                                 // the empty partial LBS
   }
   for (uint32_t q = threadIdx.x; q < p.r * ew; q += blockDim.x) {
     const uint32_t y = q / ew, w = q % ew;
-    s_bits[q] = p.sa_bits[((size_t)y * p.F + z) * ew + w];
+    s_bits[q] = __ldcg(p.sa_bits + ((size_t)y * p.F + z) * ew + w);
   }
   __syncthreads();
+  RPROF(2);
   const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t n_in = 1;
   for (uint32_t y = 0; y < p.r; ++y) {
-    const uint32_t n_in = s_nin;
     const uint32_t nsa = s_nsa[y];
     if (n_in == 0 || nsa == 0) break;                 // uniform across the CTA
-    if (threadIdx.x == 0) s_next = 0;
-    __syncthreads();
+    uint32_t* const cnt = &s_cnt[y % 3];              // zero (set two rows ago)
+    if (threadIdx.x == 0) s_cnt[(y + 1) % 3] = 0;     // next row's; last read as n_in before row y-1
     const bool last = (y + 1 == p.r);
     const uint32_t nf = p.nfree[y];
     const bool use_enum = ((1ull << nf) <= (uint64_t)p.use_enum_max[y] * nsa);
@@ -667,84 +697,115 @@ __global__ void __launch_bounds__(512, 2) k_restore(RestoreParams p) {   // 2 CT
     const uint32_t ib = y & 1u, ob = (y + 1) & 1u;
     const uint32_t* sal = p.sa_list + ((size_t)y * p.F + z) * E;
     const uint32_t* bits = s_bits + y * ew;
+    const uint32_t sh = p.shift[y], ovy = p.ov[y];
+    const uint32_t dn1 = p.dep_n1[y], ds1 = p.dep_sh1[y], ds2 = p.dep_sh2[y], dok = p.dep_ok[y];
     const uint64_t rounded = (total + 31u) & ~31ull;
     for (uint64_t idx = threadIdx.x; idx < rounded; idx += blockDim.x) {
       bool ok = false;
       uint32_t nl = 0;
       if (idx < total) {
-        const uint32_t pi = (uint32_t)(idx / per);
+        // (partial, option) of this probe: 32-bit division whenever the level fits 32 bits
+        uint32_t pi, jj;
+        if (total <= 0xFFFFFFFFull) { pi = (uint32_t)idx / (uint32_t)per; jj = (uint32_t)idx - pi * (uint32_t)per; }
+        else { pi = (uint32_t)(idx / per); jj = (uint32_t)(idx % per); }
         const uint32_t L = (pi < kPartSmem) ? s_part[ib][pi] : gbuf[ib][pi - kPartSmem];
-        const uint32_t sub = (y == 0) ? (uint32_t)(part + (idx % per) * p.parts) : (uint32_t)(idx % per);
+        const uint32_t sub = (y == 0) ? part + jj * p.parts : jj;
         const uint64_t D = (uint64_t)L | ((uint64_t)L << p.W);
-        const uint32_t xk = (uint32_t)(D >> p.shift[y]) & cmask;
+        const uint32_t xk = (uint32_t)(D >> sh) & cmask;
         uint32_t x;
         if (use_enum) {
-          x = xk & p.ov[y];
-          for (uint32_t b = 0; b < nf; ++b) x |= ((sub >> b) & 1u) << p.freepos[y][b];
+          // the completion sub's bits go to the free positions of x_y (ascending)
+          if (dok) {
+            const uint32_t m1 = (1u << dn1) - 1u;   // dn1 <= nf <= c < 32
+            x = (xk & ovy) | ((sub & m1) << ds1) | ((sub & ~m1) << ds2);
+          } else {
+            x = xk & ovy;
+            for (uint32_t b = 0; b < nf; ++b) x |= ((sub >> b) & 1u) << p.freepos[y][b];
+          }
           ok = (bits[x >> 5] >> (x & 31u)) & 1u;
         } else {
-          x = __ldcg(sal + sub);
-          ok = ((x ^ xk) & p.ov[y]) == 0;
+          x = (y == 0 && jj < 32) ? s_pre[jj] : __ldcg(sal + sub);
+          ok = ((x ^ xk) & ovy) == 0;
         }
-        nl = L | place_row(x, p.shift[y], p.W);
+        nl = L | place_row(x, sh, p.W);
       }
       // warp-aggregated append
       const uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
       if (!m) continue;
-      const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+      const uint32_t rank = __popc(m & lt);
       const uint32_t leader = __ffs(m) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(last ? p.n_cand : &s_next, __popc(m));
-      base = __shfl_sync(0xFFFFFFFFu, base, leader);
-      if (!ok) continue;
-      const uint32_t slot = base + rank;
       if (!last) {
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(cnt, __popc(m));
+        base = __shfl_sync(0xFFFFFFFFu, base, leader);
+        if (!ok) continue;
+        const uint32_t slot = base + rank;
         if (slot < kPartSmem) s_part[ob][slot] = nl;
         else if (slot < kPartSmem + p.ws_cap) gbuf[ob][slot - kPartSmem] = nl;
         else *p.overflow = 1u;
         continue;
       }
-      if (slot >= p.max_cand) { *p.overflow = 1u; continue; }
-      // a restored candidate: f(ip) = (LBS << u) | z, ip = A^{-1} f
-      const uint32_t h = (p.u ? (nl << p.u) : nl) | (p.z_base + z);
-      p.cand[slot] = h;
-      // Alg. 5 NAT: ATs active in all r ATVs of the candidate
-      const uint64_t DL = (uint64_t)nl | ((uint64_t)nl << p.W);
-      const uint4* rows[kMaxR];
+      // a restored candidate: the warp's slots are reserved first, the NAT words load while
+      // the atomic is in flight (the slot is only needed for the stores)
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(p.n_cand, __popc(m));
+      uint32_t h = 0, nat = 0, flags = 0, ip = 0;
+      double est = 0.0;
+      if (ok) {
+        // f(ip) = (LBS << u) | z, ip = A^{-1} f
+        h = (p.u ? (nl << p.u) : nl) | (p.z_base + z);
+        // Alg. 5 NAT: ATs active in all r ATVs of the candidate, 4 x 16 B of
+        // every row per batch, all loads issued before the AND (g = 512: one batch)
+        const uint64_t DL = (uint64_t)nl | ((uint64_t)nl << p.W);
+        const uint4* rows[kMaxR];
 #pragma unroll
-      for (int yy = 0; yy < kMaxR; ++yy) {
-        if (yy < (int)p.r) {
-          const uint32_t xx = (uint32_t)(DL >> p.shift[yy]) & cmask;
+        for (int yy = 0; yy < kMaxR; ++yy) {
+          const uint32_t xx = (yy < (int)p.r) ? (uint32_t)(DL >> p.shift[yy]) & cmask : 0u;
           rows[yy] = reinterpret_cast<const uint4*>(p.active + ((((size_t)yy * p.F + z) << p.c) | xx) * p.wpa);
         }
-      }
-      uint32_t nat = 0;
-      for (uint32_t w4 = 0; w4 < p.wpa / 4; ++w4) {
-        uint4 acc = __ldcg(rows[0] + w4);
+        const uint32_t nw4 = p.wpa / 4;
+        for (uint32_t w0 = 0; w0 < nw4; w0 += 4) {
+          uint4 a[4][kMaxR];
 #pragma unroll
-        for (int yy = 1; yy < kMaxR; ++yy) {
-          if (yy < (int)p.r) {
-            const uint4 b4 = __ldcg(rows[yy] + w4);
-            acc.x &= b4.x; acc.y &= b4.y; acc.z &= b4.z; acc.w &= b4.w;
+          for (int yy = 0; yy < kMaxR; ++yy)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              a[k][yy] = (yy < (int)p.r && w0 + k < nw4) ? __ldcg(rows[yy] + w0 + k)
+                                                        : make_uint4(~0u, ~0u, ~0u, ~0u);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint4 acc = a[k][0];
+#pragma unroll
+            for (int yy = 1; yy < kMaxR; ++yy) {
+              acc.x &= a[k][yy].x; acc.y &= a[k][yy].y; acc.z &= a[k][yy].z; acc.w &= a[k][yy].w;
+            }
+            if (w0 + k < nw4) nat += __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
           }
         }
-        nat += __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
+        // Eq. 5 (A19) in double; NAT == g -> +inf (A20)
+        if (nat == p.g) est = __longlong_as_double(0x7FF0000000000000LL);
+        else est = -(double)p.g * log((double)(p.g - nat) / ((double)p.g * (1.0 - s_up)));
+        flags = (nat == p.g ? 1u : 0u) | (est >= p.theta ? 2u : 0u);
+        ip = p.mangle_p ? walk_mod_p(p.A_inv, h) : (uint32_t)p.A_inv * h;   // f^{-1}
       }
-      // Eq. 5 (A19) in double; NAT == g -> +inf (A20)
-      double est;
-      if (nat == p.g) est = __longlong_as_double(0x7FF0000000000000LL);
-      else est = -(double)p.g * log((double)(p.g - nat) / ((double)p.g * (1.0 - s_up)));
-      const uint32_t flags = (nat == p.g ? 1u : 0u) | (est >= p.theta ? 2u : 0u);
-      const uint32_t ip = p.mangle_p ? walk_mod_p(p.A_inv, h) : (uint32_t)p.A_inv * h;   // f^{-1}
+      base = __shfl_sync(0xFFFFFFFFu, base, leader);
+      if (!ok) continue;
+      const uint32_t slot = base + rank;
+      if (slot >= p.max_cand) { *p.overflow = 1u; continue; }
+#ifdef ASSE_RESTORE_NO_NAT
+      continue;                                       // tools only: the join without the report stores
+#endif
+      p.cand[slot] = h;
       ReportDev* R = reinterpret_cast<ReportDev*>(p.reports) + slot;
       R->ip = ip; R->nat = nat; R->estimate = est; R->flags = flags; R->pad = 0;
       p.keys[slot] = ip;
       p.vals[slot] = slot;
     }
     __syncthreads();
-    if (threadIdx.x == 0) s_nin = (uint32_t)min((uint64_t)s_next, (uint64_t)kPartSmem + p.ws_cap);
-    __syncthreads();
+    RPROF(3 + (y < 3 ? y : 3));
+    n_in = (uint32_t)min((uint64_t)*cnt, (uint64_t)kPartSmem + p.ws_cap);   // (last row: unused)
   }
+  RPROF(7);
   if (p.sys_fence) __threadfence_system();
   pdl_trigger();
 }

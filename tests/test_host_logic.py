@@ -40,3 +40,52 @@ def test_owner_formula_exact(name, sms):
 def test_queue_ring_holds_a_round(sms):
     group = (sms + KBIN_QG - 1) // KBIN_QG           # producers per (owner, group) ring
     assert group * KBIN_CAP <= KBIN_QCAP             # a round never laps the ring
+
+
+def _freepos(c, s, u, r):
+    """Mirror of asse_init's join plan: per row y the window positions j of x_y whose LBS bit
+    (s*y + j) mod W is not fixed by rows < y."""
+    W = 32 - u
+    known = [False] * W
+    out = []
+    for y in range(r):
+        fp = [j for j in range(c) if not known[(s * y + j) % W]]
+        for j in range(c):
+            known[(s * y + j) % W] = True
+        out.append(fp)
+    return out
+
+
+def _two_runs(fp):
+    """Mirror of asse_init: (ok, n1, sh1, sh2) with bits [0, n1) << sh1, the rest << sh2."""
+    nf = len(fp)
+    n1 = 0
+    while n1 < nf and fp[n1] == fp[0] + n1:
+        n1 += 1
+    n2 = 0
+    while n1 + n2 < nf and fp[n1 + n2] == fp[n1] + n2:
+        n2 += 1
+    return n1 + n2 == nf, n1, (fp[0] if nf else 0), (fp[n1] - n1 if n1 < nf else 0)
+
+
+@pytest.mark.parametrize("c,s,u,r", [(12, 6, 4, 4), (9, 7, 4, 4), (10, 5, 4, 4), (9, 6, 3, 4), (14, 5, 4, 4),
+                                     (8, 8, 8, 4), (11, 3, 2, 8), (6, 4, 12, 4)])
+def test_restore_deposit_runs_equal_the_bit_loop(c, s, u, r):
+    """k_restore enumerates the completions of x_y by depositing the bits of sub into the free
+    positions; the two-run form (shifts of two masked parts) must equal the per-bit loop for
+    every sub < 2^nf whenever asse_init admits it (and the BASELINE geometries must admit it)."""
+    W = 32 - u
+    if c + s * (r - 1) < W:
+        pytest.skip("incomplete geometry (rejected by validate)")
+    for y, fp in enumerate(_freepos(c, s, u, r)):
+        ok, n1, sh1, sh2 = _two_runs(fp)
+        if (c, s, u) in ((12, 6, 4), (9, 7, 4)):
+            assert ok, (y, fp)
+        if not ok or len(fp) > 16:
+            continue
+        m1 = (1 << n1) - 1
+        for sub in range(1 << len(fp)):
+            loop = 0
+            for b, pos in enumerate(fp):
+                loop |= ((sub >> b) & 1) << pos
+            assert ((sub & m1) << sh1) | ((sub & ~m1) << sh2) == loop
