@@ -654,6 +654,10 @@ __global__ void __launch_bounds__(512, 2) k_restore(RestoreParams p) {   // 2 CT
   RPROF(0);
   pdl_wait();                                         // k_fold's SA lists, bits, AAT, active bits
   RPROF(1);
+#ifdef ASSE_RESTORE_EMPTY
+  pdl_trigger();                                      // tools only: the restore's share of the step
+  return;
+#endif
   // prologue, one round trip: |SA(y, z)|, row 0's prefetched options, UP, the SA bits
   if (threadIdx.x < p.r) s_nsa[threadIdx.x] = __ldcg(p.sa_cnt + threadIdx.x * p.F + z);
   if (threadIdx.x >= 32 && threadIdx.x < 64) {
@@ -679,6 +683,10 @@ __global__ void __launch_bounds__(512, 2) k_restore(RestoreParams p) {   // 2 CT
   }
   __syncthreads();
   RPROF(2);
+#ifdef ASSE_RESTORE_PROLOGUE_ONLY
+  pdl_trigger();                                      // tools only: launch + prologue share
+  return;
+#endif
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t n_in = 1;
@@ -833,6 +841,9 @@ __global__ void __launch_bounds__(kSortThreads) k_sort(const ReportDev* __restri
   // slice are complete), so no host-to-device copy precedes the next end_slice
   if (clock && blockIdx.x == 0 && threadIdx.x == 0) *clock = (*clock + 1u == two_k) ? 0u : *clock + 1u;
   const uint32_t n = min(*n_ptr, max_cand);
+#ifdef ASSE_SORT_EMPTY
+  return;                                              // tools only: the sort's share of the step
+#endif
   if (n == 0) return;
   if (n > kRankCap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) counters[5] = 1u;
