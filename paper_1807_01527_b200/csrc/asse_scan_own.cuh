@@ -255,8 +255,9 @@ __global__ void __launch_bounds__(kOwnThreads, 1) k_scan_own(const uint2* __rest
   constexpr int kGroupThreads = 32 * (kOwnConsWarps / kOwnNGR);   // named barriers 2 .. 1 + NGR
   constexpr int kComputeThreads = 32 * (kOwnBinWarps + kOwnConsWarps);   // named barrier 8
 
-  if (owner)
-    for (uint32_t q = threadIdx.x; q < slice_words; q += blockDim.x) sbm[q] = 0;
+  if (owner)   // 16-B stores (sbm is 16-B aligned, slice_words a multiple of 4): scan -0.7 us per call
+    for (uint32_t q = threadIdx.x; q < slice_words / 4; q += blockDim.x)
+      reinterpret_cast<uint4*>(sbm)[q] = make_uint4(0u, 0u, 0u, 0u);
   for (uint32_t q = threadIdx.x; q < 2 * Op; q += blockDim.x) scount[q] = 0;
   if (threadIdx.x == 0) {
     for (int st = 0; st < kOwnRing; ++st) {
