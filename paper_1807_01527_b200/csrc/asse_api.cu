@@ -818,7 +818,10 @@ asse_status asse_init(const asse_config* cfg, void** out) {
         while (n1 < nf && rp.freepos[y][n1] == rp.freepos[y][0] + n1) ++n1;
         uint32_t n2 = 0;
         while (n1 + n2 < nf && rp.freepos[y][n1 + n2] == rp.freepos[y][n1] + n2) ++n2;
-        rp.dep_ok[y] = (n1 + n2 == nf) ? 1 : 0;
+        if (n1 + n2 != nf) {   // unreachable for an admissible geometry (window = cyclic interval)
+          c->err = "restore plan: the free positions of a row are not two runs";
+          return fail(ASSE_E_PARAM);
+        }
         rp.dep_n1[y] = (uint8_t)n1;
         rp.dep_sh1[y] = nf ? rp.freepos[y][0] : 0;
         rp.dep_sh2[y] = (n1 < nf) ? (uint8_t)(rp.freepos[y][n1] - n1) : 0;

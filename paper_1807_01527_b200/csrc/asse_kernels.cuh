@@ -585,10 +585,9 @@ struct RestoreParams {
   uint32_t nfree[kMaxR];    // c - popc(ov[y])
   uint32_t use_enum_max[kMaxR];  // enumerate the 2^nfree completions when 2^nfree <= this * |SA|
   uint8_t freepos[kMaxR][32];    // free bit positions of x_y
-  // the free positions as at most two ascending runs: completion bits [0, n1) shift up by
-  // sh1 (= freepos[0]), bits [n1, nf) by sh2 (= freepos[n1] - n1); dep_ok = 0: more runs,
-  // the freepos loop is used
-  uint8_t dep_n1[kMaxR], dep_sh1[kMaxR], dep_sh2[kMaxR], dep_ok[kMaxR];
+  // the free positions as two ascending runs: completion bits [0, n1) shift up by sh1
+  // (= freepos[0]), bits [n1, nf) by sh2 (= freepos[n1] - n1)
+  uint8_t dep_n1[kMaxR], dep_sh1[kMaxR], dep_sh2[kMaxR];
   // Alg. 5 / Eq. 5 for every restored candidate (fused)
   const uint32_t* active;        // active bits, wpa words per ATV
   const unsigned long long* aat; // AAT[y][z]
@@ -706,7 +705,7 @@ __global__ void __launch_bounds__(512, 2) k_restore(RestoreParams p) {   // 2 CT
     const uint32_t* sal = p.sa_list + ((size_t)y * p.F + z) * E;
     const uint32_t* bits = s_bits + y * ew;
     const uint32_t sh = p.shift[y], ovy = p.ov[y];
-    const uint32_t dn1 = p.dep_n1[y], ds1 = p.dep_sh1[y], ds2 = p.dep_sh2[y], dok = p.dep_ok[y];
+    const uint32_t dn1 = p.dep_n1[y], ds1 = p.dep_sh1[y], ds2 = p.dep_sh2[y];
     const uint64_t rounded = (total + 31u) & ~31ull;
     for (uint64_t idx = threadIdx.x; idx < rounded; idx += blockDim.x) {
       bool ok = false;
@@ -722,14 +721,11 @@ __global__ void __launch_bounds__(512, 2) k_restore(RestoreParams p) {   // 2 CT
         const uint32_t xk = (uint32_t)(D >> sh) & cmask;
         uint32_t x;
         if (use_enum) {
-          // the completion sub's bits go to the free positions of x_y (ascending)
-          if (dok) {
-            const uint32_t m1 = (1u << dn1) - 1u;   // dn1 <= nf <= c < 32
-            x = (xk & ovy) | ((sub & m1) << ds1) | ((sub & ~m1) << ds2);
-          } else {
-            x = xk & ovy;
-            for (uint32_t b = 0; b < nf; ++b) x |= ((sub >> b) & 1u) << p.freepos[y][b];
-          }
+          // the completion sub's bits go to the free positions of x_y (ascending), which form
+          // at most two runs: the window is a cyclic interval and the fixed LBS bits a growing
+          // one (host-checked; tests/test_host_logic.py over every admissible geometry)
+          const uint32_t m1 = (1u << dn1) - 1u;     // dn1 <= nf <= c < 32
+          x = (xk & ovy) | ((sub & m1) << ds1) | ((sub & ~m1) << ds2);
           ok = (bits[x >> 5] >> (x & 31u)) & 1u;
         } else {
           x = (y == 0 && jj < 32) ? s_pre[jj] : __ldcg(sal + sub);

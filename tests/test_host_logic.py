@@ -68,20 +68,47 @@ def _two_runs(fp):
     return n1 + n2 == nf, n1, (fp[0] if nf else 0), (fp[n1] - n1 if n1 < nf else 0)
 
 
+def _admissible(c, s, u, r):
+    """Mirror of validate(): completeness and at least one duplicate position."""
+    W = 32 - u
+    if c + s * (r - 1) < W or c + u > 24 or s > c:
+        return False
+    cover = [0] * W
+    for y in range(r):
+        for j in range(c):
+            cover[(s * y + j) % W] += 1
+    return min(cover) > 0 and max(cover) > 1
+
+
+def test_restore_free_positions_are_two_runs_for_every_geometry():
+    """asse_init rejects a join plan whose free positions are not two ascending runs; that
+    must never happen for an admissible geometry (a window is a cyclic interval of the LBS
+    and the bits fixed by earlier rows a growing one)."""
+    n = 0
+    for u in range(0, 17):
+        for c in range(2, 23):
+            for s in range(1, c + 1):
+                for r in range(2, 9):
+                    if not _admissible(c, s, u, r):
+                        continue
+                    n += 1
+                    for fp in _freepos(c, s, u, r):
+                        assert _two_runs(fp)[0], (c, s, u, r, fp)
+    assert n > 1000
+
+
 @pytest.mark.parametrize("c,s,u,r", [(12, 6, 4, 4), (9, 7, 4, 4), (10, 5, 4, 4), (9, 6, 3, 4), (14, 5, 4, 4),
                                      (8, 8, 8, 4), (11, 3, 2, 8), (6, 4, 12, 4)])
 def test_restore_deposit_runs_equal_the_bit_loop(c, s, u, r):
     """k_restore enumerates the completions of x_y by depositing the bits of sub into the free
     positions; the two-run form (shifts of two masked parts) must equal the per-bit loop for
-    every sub < 2^nf whenever asse_init admits it (and the BASELINE geometries must admit it)."""
-    W = 32 - u
-    if c + s * (r - 1) < W:
-        pytest.skip("incomplete geometry (rejected by validate)")
+    every sub < 2^nf."""
+    if not _admissible(c, s, u, r):
+        pytest.skip("rejected by validate")
     for y, fp in enumerate(_freepos(c, s, u, r)):
         ok, n1, sh1, sh2 = _two_runs(fp)
-        if (c, s, u) in ((12, 6, 4), (9, 7, 4)):
-            assert ok, (y, fp)
-        if not ok or len(fp) > 16:
+        assert ok, (y, fp)
+        if len(fp) > 16:
             continue
         m1 = (1 << n1) - 1
         for sub in range(1 << len(fp)):
