@@ -28,7 +28,8 @@ def build(force=False, verbose=False):
 def build_variant(out_path, defines=(), verbose=False):
     """Build libasse with extra -D defines into out_path (tools/sweep.py). Never touches
     the product library."""
-    cmd = [NVCC, *FLAGS, "-shared", "-I", os.path.join(ROOT, "include"),
+    extra = os.environ.get("ASSE_NVCC_EXTRA", "").split()   # tools only: compiler-option sweeps
+    cmd = [NVCC, *FLAGS, *extra, "-shared", "-I", os.path.join(ROOT, "include"),
            *["-D" + d for d in defines], os.path.join(PKG, "csrc", "asse_api.cu"), "-o", out_path + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
