@@ -195,3 +195,19 @@ def test_state_machine_errors(cuda_device):
     with pytest.raises(asse.AsseError):
         asse.Asse(**dict(PRESETS["C1"], g=100))
 
+
+
+@pytest.mark.parametrize("k,T", [(63, 2 * 63 + 3), (64, 2 * 64 + 3), (16383, 6)])
+def test_code_width_boundaries_and_max_k(cuda_device, k, T):
+    """Code-width edges (A2): k = 63 is the largest window with 8-bit codes (2k = 126, the
+    EMPTY value 2k still below the guard bit), k = 64 the first with 16-bit codes; both run
+    past their erasures (t >= k) and the C0 wrap (t = 2k). k = 16383 is validate()'s maximum
+    (15-bit device codes): with g = 256 < 2k every AT sits in block 2k-1 (A7), so the block
+    ACT starts at 2k-1 = 32765 and the checkAT intervals wrap from the first slice."""
+    geo = dict(k=k, r=4, c=8, u=4, s=7, g=256, theta=300.0, seed=41)
+    dev, ora = asse.Asse(**geo), O.Oracle(**geo)
+    assert dev.stats()["code_bytes"] == (1 if 2 * k <= 126 else 2)
+    gen = Generator("C2", N=30_000)
+    for t in range(T):
+        step_both(dev, ora, gen.slice(t), geo["theta"], "k=%d t=%d" % (k, t))
+    assert dev.clock() == (T, T % (2 * k))
