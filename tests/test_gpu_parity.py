@@ -211,3 +211,22 @@ def test_code_width_boundaries_and_max_k(cuda_device, k, T):
     for t in range(T):
         step_both(dev, ora, gen.slice(t), geo["theta"], "k=%d t=%d" % (k, t))
     assert dev.clock() == (T, T % (2 * k))
+
+
+@pytest.mark.parametrize("r,c,u,s", [(2, 15, 4, 13), (3, 12, 4, 8), (5, 9, 2, 6), (8, 8, 4, 3), (4, 12, 0, 7),
+                                     (4, 6, 12, 5)])
+def test_row_counts_and_frame_extremes(cuda_device, r, c, u, s):
+    """Geometries off the BASELINE shape (validate()'s range): r = 2, 3, 5 and 8
+    rows (the scan falls back to k_scan, which handles any r; the fold and the join are
+    generic in r), a single frame (u = 0, 32-bit LBS) and 4096 frames of 64 estimators
+    (u = 12). C1's planted super points make CSIP non-empty; pool, CSIP, NAT and the
+    estimates equal the oracle after every slice past the first erasures (k = 4)."""
+    geo = dict(k=4, r=r, c=c, u=u, s=s, g=256, theta=1024.0, seed=43)
+    dev, ora = asse.Asse(**geo), O.Oracle(**geo)
+    gen = Generator("C1")
+    seen = 0
+    for t in range(10):
+        rep_d, _ = step_both(dev, ora, gen.slice(t), geo["theta"], "r=%d c=%d u=%d t=%d" % (r, c, u, t))
+        seen += len(rep_d)
+    assert seen > 0                                   # the join produced candidates
+    assert dev.stats()["scan_own_launches"] == 0 or r == 4
